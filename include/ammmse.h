@@ -1,0 +1,158 @@
+/*
+ * ammmse.h — C-ABI of the B200-native batched A-MMMSE engine (libammmse.so).
+ *
+ * One call solves B independent channel realizations of the weighted
+ * sum-rate precoder problem with the A-MMMSE algorithm (arXiv 2510.20507),
+ * i.e. it replaces, per realization, the reference call
+ *
+ *     wsrbeam.run_ammmse(channels, config, options) -> SolveResult
+ *         pkg/src/wsrbeam/solvers.py:540-550  (driver)
+ *         pkg/src/wsrbeam/solvers.py:415-518  (_run_bcd loop, exact=False,
+ *                                              use_extrapolation=True,
+ *                                              start_weighted=False)
+ *
+ * and its once-per-solve helper
+ *
+ *     wsrbeam.compute_bounds(channels, weights, p_max, noise_power)
+ *         pkg/src/wsrbeam/objective.py:216-240
+ *
+ * The reference is pure Python (no FFI exists upstream); the binding a
+ * maintainer would add on the reference side is a ctypes stub, shown in
+ * INTEGRATION.md.  Signatures carry plain pointers and sizes only.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers on the current CUDA device.
+ *   - Complex arrays are interleaved (re, im) pairs: complex64 = 2 x float,
+ *     complex128 = 2 x double (numpy / torch memory layout).
+ *   - Layouts follow the reference containers: channels (B, K, N, M)
+ *     (model.py:110), precoders (B, K, M, d) (model.py:141).
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     stream-ordered and asynchronous.  No global mutable state: calls are
+ *     reentrant across streams and devices.
+ *   - Return value: 0 on success, a negative AMMMSE_ERR_* code otherwise.
+ *     Numerical failures of individual realizations are NOT call errors:
+ *     they are reported per realization in `status` (AMMMSE_STATUS_*), the
+ *     way the reference harness records per-realization exceptions
+ *     (harness.py:277-278).
+ */
+#ifndef AMMMSE_H_
+#define AMMMSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMMMSE_ABI_VERSION 1
+
+/* element type of channels / precoders */
+enum {
+  AMMMSE_COMPLEX64 = 0,  /* fp32 GEMMs, fp64 small algebra + WSR */
+  AMMMSE_COMPLEX128 = 1  /* fp64 throughout (reference precision, model.py:93) */
+};
+
+/* call status */
+enum {
+  AMMMSE_OK = 0,
+  AMMMSE_ERR_INVALID = -1,      /* bad pointer / dims / options (ConfigError) */
+  AMMMSE_ERR_UNSUPPORTED = -2,  /* shape not instantiated (N or d > 4, SMEM) */
+  AMMMSE_ERR_WORKSPACE = -3,    /* workspace NULL or smaller than ammmse_workspace_size */
+  AMMMSE_ERR_CUDA = -4          /* a CUDA runtime call failed */
+};
+
+/* per-realization status (result.status) */
+enum {
+  AMMMSE_STATUS_OK = 0,              /* converged or reached max_iters */
+  AMMMSE_STATUS_ILL_CONDITIONED = 1, /* IllConditionedWeightError, solvers.py:243-252 */
+  AMMMSE_STATUS_UNSTABLE = 2,        /* UnstableParametersError, solvers.py:490-500 */
+  AMMMSE_STATUS_NONFINITE = 3        /* non-finite iterate / failed Cholesky */
+};
+
+/* trace record fields, in IterationRecord order (solvers.py:139-156) */
+enum {
+  AMMMSE_TRACE_T = 0, AMMMSE_TRACE_WSR_BITS, AMMMSE_TRACE_F_VALUE,
+  AMMMSE_TRACE_TOTAL_POWER, AMMMSE_TRACE_STAGE, AMMMSE_TRACE_F_AFTER_U,
+  AMMMSE_TRACE_F_AFTER_W, AMMMSE_TRACE_F_AFTER_V, AMMMSE_TRACE_REL_CHANGE,
+  AMMMSE_TRACE_FIELDS
+};
+
+typedef struct AmmmseDims {
+  int64_t batch;  /* B, number of realizations (>= 1) */
+  int32_t M;      /* BS antennas */
+  int32_t N;      /* receive antennas per user (1..4) */
+  int32_t K;      /* users */
+  int32_t d;      /* streams per user (1..4) */
+  int32_t dtype;  /* AMMMSE_COMPLEX64 | AMMMSE_COMPLEX128 */
+} AmmmseDims;
+
+/* inputs (ChannelSet + SystemConfig + V0 of each realization) */
+typedef struct AmmmseProblem {
+  const void* channels;        /* (B, K, N, M) complex                         */
+  const double* noise_power;   /* (B,)   sigma^2 > 0      (ChannelSet.noise_power) */
+  const double* p_max;         /* (B,)   P > 0            (SystemConfig.p_max)     */
+  const double* weights;       /* (B, K) alpha_k > 0      (SystemConfig.weights)   */
+  const void* init_precoders;  /* (B, K, M, d) complex, V0 (init_precoders(), model.py:225-235) */
+} AmmmseProblem;
+
+/* SolverOptions (solvers.py:88-136) after resolve_step_parameters (:196-207) */
+typedef struct AmmmseOptions {
+  double gamma;        /* step size, used when gamma_safe == 0 (> 0, finite)           */
+  int32_t gamma_safe;  /* 1: gamma = per-realization gamma_safe (GAMMA_SAFE sentinel)  */
+  int32_t max_iters;   /* >= 1                                                         */
+  double omega;        /* extrapolation, [0, 1)                                        */
+  double eps1;         /* stage-switch threshold, > 0, may be +inf                     */
+  double eps2;         /* stop threshold, > 0, finite, <= eps1                         */
+  int32_t latch_stage; /* 1: latch the weighted stage (default); 0: re-test every iteration */
+  int32_t reserved;
+} AmmmseOptions;
+
+/* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */
+typedef struct AmmmseResult {
+  void* final_precoders;          /* (B, K, M, d) complex, same dtype as inputs    */
+  double* wsr_bits;               /* (B,)  trace[-1].wsr_bits                      */
+  int32_t* iterations;            /* (B,)  len(trace)                              */
+  uint8_t* converged;             /* (B,)                                          */
+  double* stationarity_residual;  /* (B,)                                          */
+  int32_t* switch_iteration;      /* (B,)  first weighted iteration, -1 = None     */
+  int32_t* status;                /* (B,)  AMMMSE_STATUS_*                         */
+  double* gamma_used;             /* (B,)  resolved step size                      */
+  double* trace;                  /* (B, max_iters, AMMMSE_TRACE_FIELDS), rows past
+                                     `iterations` are left untouched              */
+} AmmmseResult;
+
+/* BoundsReport (objective.py:40-66) per realization, (B, 5) row-major */
+enum {
+  AMMMSE_BOUND_KAPPA = 0, AMMMSE_BOUND_L_V, AMMMSE_BOUND_GAMMA_SAFE,
+  AMMMSE_BOUND_EK_FLOOR, AMMMSE_BOUND_ALPHA_BAR, AMMMSE_BOUND_FIELDS
+};
+
+/* ABI version (AMMMSE_ABI_VERSION) */
+int ammmse_abi_version(void);
+
+/* 0 if the dims are supported by the compiled engine, else AMMMSE_ERR_* */
+int ammmse_check_dims(const AmmmseDims* dims);
+
+/* bytes of device workspace ammmse_solve needs (0 on invalid dims) */
+size_t ammmse_workspace_size(const AmmmseDims* dims);
+
+/* Solve all B realizations.  Replaces run_ammmse (solvers.py:540-550). */
+int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* problem,
+                 const AmmmseOptions* options, AmmmseResult* result,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Spectral bounds.  Replaces compute_bounds (objective.py:216-240).
+   out: device (B, AMMMSE_BOUND_FIELDS) doubles. */
+int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* weights,
+                  const double* p_max, const double* noise_power, double* out, void* stream);
+
+/* Human-readable text for an AMMMSE_ERR_* code, plus the last CUDA error of
+   this thread if any. */
+const char* ammmse_error_string(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMMMSE_H_ */

@@ -1,0 +1,222 @@
+// ammmse_capi.cu — extern "C" boundary of libammmse.so (include/ammmse.h).
+//
+// Validation mirrors the reference's construction-time checks:
+//   SolverOptions.__post_init__  (pkg/src/wsrbeam/solvers.py:109-136)
+//   SystemConfig.__post_init__   (pkg/src/wsrbeam/model.py:60-85)
+// Per-array value checks (finite entries, sigma^2 > 0, alpha > 0) are the
+// host layer's job (it owns the host copies); the ABI checks shapes, pointers
+// and option ranges.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "ammmse.h"
+#include "ammmse_engine.cuh"
+#include "entries.h"
+
+namespace {
+
+thread_local char g_err[256];
+
+const ammmse::KernelEntry* lookup(const AmmmseDims* d) {
+  if (d->N < 1 || d->N > 4 || d->d < 1 || d->d > 4) return nullptr;
+  const ammmse::KernelEntry* t = nullptr;
+  if (d->dtype == AMMMSE_COMPLEX64) {
+    switch (d->N) {
+      case 1: t = ammmse::entries_float_1(); break;
+      case 2: t = ammmse::entries_float_2(); break;
+      case 3: t = ammmse::entries_float_3(); break;
+      case 4: t = ammmse::entries_float_4(); break;
+    }
+  } else if (d->dtype == AMMMSE_COMPLEX128) {
+    switch (d->N) {
+      case 1: t = ammmse::entries_double_1(); break;
+      case 2: t = ammmse::entries_double_2(); break;
+      case 3: t = ammmse::entries_double_3(); break;
+      case 4: t = ammmse::entries_double_4(); break;
+    }
+  }
+  return t ? &t[d->d - 1] : nullptr;
+}
+
+int dims_valid(const AmmmseDims* d) {
+  if (!d) return AMMMSE_ERR_INVALID;
+  if (d->batch < 1 || d->M < 1 || d->N < 1 || d->K < 1 || d->d < 1) return AMMMSE_ERR_INVALID;
+  if (d->dtype != AMMMSE_COMPLEX64 && d->dtype != AMMMSE_COMPLEX128) return AMMMSE_ERR_INVALID;
+  return AMMMSE_OK;
+}
+
+int max_smem_optin() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  return v;
+}
+
+// Threads per CTA: about one 2x2 output tile of the larger GEMM per thread,
+// 64..256, multiple of 32.
+int pick_threads(const AmmmseDims* d) {
+  const long tiles_a = (long)((d->M + 1) / 2) * (((long)d->K * d->d + 1) / 2);
+  const long tiles_b = (long)((d->K * d->N + 1) / 2) * (((long)d->K * d->d + 1) / 2);
+  long t = tiles_a > tiles_b ? tiles_a : tiles_b;
+  t = (t + 31) / 32 * 32;
+  if (t < 64) t = 64;
+  if (t > 256) t = 256;
+  return (int)t;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+  return AMMMSE_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ammmse_abi_version(void) { return AMMMSE_ABI_VERSION; }
+
+int ammmse_check_dims(const AmmmseDims* dims) {
+  int rc = dims_valid(dims);
+  if (rc) return rc;
+  const ammmse::KernelEntry* e = lookup(dims);
+  if (!e) return AMMMSE_ERR_UNSUPPORTED;
+  const size_t need = e->smem_bytes(dims->M, dims->K);
+  // 227 KB is the sm_100 opt-in limit; without a device we cannot query it.
+  int lim = max_smem_optin();
+  if (lim <= 0) lim = 232448;
+  if (need > (size_t)lim) return AMMMSE_ERR_UNSUPPORTED;
+  return AMMMSE_OK;
+}
+
+size_t ammmse_workspace_size(const AmmmseDims* dims) {
+  if (dims_valid(dims)) return 0;
+  return 256;  // work counter, padded
+}
+
+int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const AmmmseOptions* opt,
+                 AmmmseResult* res, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = ammmse_check_dims(dims);
+  if (rc) {
+    snprintf(g_err, sizeof g_err, "unsupported or invalid dims");
+    return rc;
+  }
+  if (!prob || !opt || !res || !prob->channels || !prob->noise_power || !prob->p_max ||
+      !prob->weights || !prob->init_precoders) {
+    snprintf(g_err, sizeof g_err, "null problem/options/result pointer");
+    return AMMMSE_ERR_INVALID;
+  }
+  // SolverOptions checks (solvers.py:112-132)
+  if (!opt->gamma_safe && !(isfinite(opt->gamma) && opt->gamma > 0)) {
+    snprintf(g_err, sizeof g_err, "gamma must be positive, got %g", opt->gamma);
+    return AMMMSE_ERR_INVALID;
+  }
+  if (!(opt->omega >= 0.0 && opt->omega < 1.0)) {
+    snprintf(g_err, sizeof g_err, "omega must lie in [0, 1), got %g", opt->omega);
+    return AMMMSE_ERR_INVALID;
+  }
+  if (!(opt->eps1 > 0)) {
+    snprintf(g_err, sizeof g_err, "eps1 must be positive");
+    return AMMMSE_ERR_INVALID;
+  }
+  if (!(opt->eps2 > 0 && isfinite(opt->eps2)) || opt->eps2 > opt->eps1) {
+    snprintf(g_err, sizeof g_err, "eps2 must be positive, finite and <= eps1");
+    return AMMMSE_ERR_INVALID;
+  }
+  if (opt->max_iters < 1) {
+    snprintf(g_err, sizeof g_err, "max_iters must be at least 1");
+    return AMMMSE_ERR_INVALID;
+  }
+  if (!workspace || workspace_bytes < ammmse_workspace_size(dims)) {
+    snprintf(g_err, sizeof g_err, "workspace missing or too small");
+    return AMMMSE_ERR_WORKSPACE;
+  }
+  const ammmse::KernelEntry* e = lookup(dims);
+  const size_t smem = e->smem_bytes(dims->M, dims->K);
+  const int threads = pick_threads(dims);
+  cudaStream_t s = (cudaStream_t)stream;
+
+  cudaError_t ce = cudaFuncSetAttribute(e->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaFuncSetAttribute");
+  int per_sm = 0;
+  ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->solve, threads, smem);
+  if (ce != cudaSuccess) return cuda_fail(ce, "occupancy");
+  if (per_sm < 1) {
+    snprintf(g_err, sizeof g_err, "kernel does not fit on an SM (smem %zu)", smem);
+    return AMMMSE_ERR_UNSUPPORTED;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long grid = (long long)sms * per_sm;
+  if (grid > dims->batch) grid = dims->batch;
+
+  ce = cudaMemsetAsync(workspace, 0, 8, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
+
+  ammmse::EngineArgs a;
+  memset(&a, 0, sizeof a);
+  a.H = prob->channels;
+  a.sigma2 = prob->noise_power;
+  a.pmax = prob->p_max;
+  a.alpha = prob->weights;
+  a.V0 = prob->init_precoders;
+  a.Vout = res->final_precoders;
+  a.wsr_bits = res->wsr_bits;
+  a.iterations = res->iterations;
+  a.converged = res->converged;
+  a.residual = res->stationarity_residual;
+  a.switch_it = res->switch_iteration;
+  a.status = res->status;
+  a.gamma_used = res->gamma_used;
+  a.trace = res->trace;
+  a.gamma = opt->gamma;
+  a.gamma_safe = opt->gamma_safe ? 1 : 0;
+  a.omega = opt->omega;
+  a.eps1 = opt->eps1;
+  a.eps2 = opt->eps2;
+  a.max_iters = opt->max_iters;
+  a.latch = opt->latch_stage ? 1 : 0;
+  a.M = dims->M;
+  a.K = dims->K;
+  a.B = dims->batch;
+  a.counter = reinterpret_cast<unsigned long long*>(workspace);
+  void* args[] = {&a};
+  ce = cudaLaunchKernel(e->solve, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaLaunchKernel(solve)");
+  return AMMMSE_OK;
+}
+
+int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* weights,
+                  const double* p_max, const double* noise_power, double* out, void* stream) {
+  int rc = dims_valid(dims);
+  if (rc) return rc;
+  const ammmse::KernelEntry* e = lookup(dims);
+  if (!e) return AMMMSE_ERR_UNSUPPORTED;
+  if (dims->K > 1024) return AMMMSE_ERR_UNSUPPORTED;
+  if (!channels || !weights || !p_max || !noise_power || !out) return AMMMSE_ERR_INVALID;
+  const void* H = channels;
+  int M = dims->M, K = dims->K;
+  long long B = dims->batch;
+  void* args[] = {(void*)&H, (void*)&weights, (void*)&p_max, (void*)&noise_power, &M, &K, &B, &out};
+  cudaError_t ce = cudaLaunchKernel(e->bounds, dim3((unsigned)B), dim3(128), args, 0, (cudaStream_t)stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaLaunchKernel(bounds)");
+  return AMMMSE_OK;
+}
+
+const char* ammmse_error_string(int code) {
+  static thread_local char buf[384];
+  const char* base = "unknown error";
+  switch (code) {
+    case AMMMSE_OK: base = "ok"; break;
+    case AMMMSE_ERR_INVALID: base = "invalid argument"; break;
+    case AMMMSE_ERR_UNSUPPORTED: base = "unsupported shape"; break;
+    case AMMMSE_ERR_WORKSPACE: base = "workspace too small"; break;
+    case AMMMSE_ERR_CUDA: base = "CUDA error"; break;
+  }
+  snprintf(buf, sizeof buf, "%s%s%s", base, g_err[0] ? ": " : "", g_err);
+  return buf;
+}
+
+}  // extern "C"

@@ -1,0 +1,990 @@
+// ammmse_engine.cuh — B200 persistent fused A-MMMSE solver.
+//
+// One CTA owns one channel realization at a time and runs the whole
+// block-coordinate loop of the reference driver (pkg/src/wsrbeam/solvers.py
+// _run_bcd :415-518 with exact=False, use_extrapolation=True,
+// start_weighted=False) with every operand resident in shared memory:
+//
+//   H (KN x M), V_cur / V_old (M x Kd), G_cur / G_old (KN x Kd, G = H V).
+//
+// CTAs pull realization indices from an atomic counter (persistent grid,
+// load-balances the per-realization iteration counts) and exit the loop of
+// a realization as soon as it stops: finished problems issue no more work.
+//
+// Per iteration (all identities are exact rewrites of the reference blocks,
+// SURVEY.md Appendix A):
+//   Ĝ  = G + ω (G − G_old)                        extrapolate (solvers.py:380-390) by linearity
+//   A_k = σ²I + Σ_j Ĝ_kj Ĝ_kj^H  (fp64)             update_receivers q-gram (:216-224)
+//   U_k = A_k^{-1} Ĝ_kk  (fp64 Cholesky)            update_receivers (:210-225)
+//   W_k = herm((I − U_k^H Ĝ_kk)^{-1}) or I          update_weight_matrices (:228-254) / stage latch (:449-464)
+//   Ŷ_m = α_m U_m W_m (U_m^H Ĝ_m − S_m)             gradient factor (objective.py:172-213) in factored form
+//   X   = V̂ − γ · 2 H^H Ŷ                           pgd_precoder_step (solvers.py:358-377)     [GEMM-A]
+//   V   = X · min(1, sqrt(P/‖X‖²))                  project_sum_power (:257-263)
+//   G   = H V                                       [GEMM-B]
+//   WSR = Σ α_k (ln det(σ²I+Σ_j G G^H) − ln det(σ²I+Σ_{j≠k} G G^H))   (objective.py:108-148), fp64
+//   f_after_u/w/v from the same Grams               wmmse_objective (objective.py:151-169)
+//   rel / switch / stop / divergence                (solvers.py:449-505)
+// Exit: stationarity residual with fresh U/W and γ_safe (solvers.py:400-412).
+//
+// Precision: GEMMs in R (fp32 for complex64 inputs, fp64 for complex128);
+// every Gram, Cholesky, log-det, objective and WSR accumulation in fp64.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ammmse.h"
+#include "small_linalg.cuh"
+
+namespace ammmse {
+
+constexpr int kMaxThreads = 256;
+constexpr int kTraceFields = AMMMSE_TRACE_FIELDS;
+constexpr double kCondLimit = 1e12;  // solvers.py:71
+constexpr double kLn2 = 0.69314718055994530942;
+
+template <typename R>
+struct RC {  // interleaved complex element of the external arrays
+  R r, i;
+};
+
+// Kernel arguments (by value).
+struct EngineArgs {
+  const void* H;
+  const double* sigma2;
+  const double* pmax;
+  const double* alpha;
+  const void* V0;
+  void* Vout;
+  double* wsr_bits;
+  int* iterations;
+  unsigned char* converged;
+  double* residual;
+  int* switch_it;
+  int* status;
+  double* gamma_used;
+  double* trace;
+  double gamma;
+  double omega, eps1, eps2;
+  int gamma_safe;
+  int max_iters;
+  int latch;
+  int M, K;
+  long long B;
+  unsigned long long* counter;
+};
+
+// Shared-memory layout of one realization, computed identically on host and
+// device.  R region (planar re/im): H, V[2], G[2], then per-user U/P/D in R;
+// fp64 region: per-user Grams, U/W caches, objective terms, reductions.
+template <typename R, int NN, int DD>
+struct Layout {
+  int M, K, KN, KD, ldh, ldv, ldg;
+  size_t nH, nV, nG;             // elements per plane
+  size_t oH, oV0, oV1, oG0, oG1; // element offsets (R) of the re planes
+  size_t oUPD;                   // element offset (R) of U|P|D small arrays
+  size_t dbl_off;                // byte offset of fp64 region
+  size_t bytes;
+
+  __host__ __device__ void init(int M_, int K_) {
+    M = M_;
+    K = K_;
+    KN = K * NN;
+    KD = K * DD;
+    // odd leading dimension for H: GEMM-B reads H down a column of k-steps
+    // from several rows at once; an odd stride spreads them over banks
+    ldh = M | 1;
+    ldv = KD;
+    ldg = KD;
+    nH = (size_t)KN * ldh;
+    nV = (size_t)M * ldv;
+    nG = (size_t)KN * ldg;
+    oH = 0;
+    oV0 = oH + 2 * nH;
+    oV1 = oV0 + 2 * nV;
+    oG0 = oV1 + 2 * nV;
+    oG1 = oG0 + 2 * nG;
+    oUPD = oG1 + 2 * nG;
+    size_t nR = oUPD + (size_t)3 * 2 * K * NN * DD;
+    dbl_off = ((nR * sizeof(R)) + 15) & ~(size_t)15;
+    bytes = dbl_off + dbl_bytes();
+  }
+  // fp64 region, in doubles:
+  //   gram   K*NN*NN cd   (2 doubles each)
+  //   ucache K*NN*DD cd
+  //   wcache K*DD*DD cd
+  //   lndetw K
+  //   alpha  K
+  //   fu fw fv rate  4K
+  //   ustat  K (stored as double)
+  //   red    32
+  __host__ __device__ size_t dbl_count() const {
+    return (size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + K + K + 4 * K + K + 32;
+  }
+  __host__ __device__ size_t dbl_bytes() const { return dbl_count() * sizeof(double); }
+};
+
+// Control block of the running realization (static shared memory).
+struct Ctl {
+  double sigma2, pmax, gamma, gamma_safe, omega, step;
+  double wsr_last, wsr_prev;  // last two completed WSR values (nats)
+  int nhist;
+  double running_max;
+  int drop_streak;
+  int latched, switch_it, weighted_now, last_weighted;
+  int cur;        // index of the current V/G buffers
+  int stop, status, converged, iters;
+  double f_u, f_w, f_v, wsr;
+  double scale, total_power;
+};
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum returned to every thread (fixed tree + fixed
+// warp order), so every thread derives bit-identical control decisions.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_allsum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory complex GEMM, planar operands, fp accumulate in R.
+//   C(p, q) = sum_k A(p, k) * B(k, q)
+//   A(p, k) = CONJT ? conj(A[k*lda + p]) : A[p*lda + k]
+//   B(k, q) = B[k*ldb + q]
+// Each thread owns RY x RX output tiles; lanes of a warp walk consecutive q
+// tiles so B reads are contiguous and A reads broadcast.
+// ---------------------------------------------------------------------------
+template <typename R, int RY, int RX, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_smem(int P, int Q, int KD, const R* __restrict__ Ar,
+                                           const R* __restrict__ Ai, int lda,
+                                           const R* __restrict__ Br, const R* __restrict__ Bi,
+                                           int ldb, Epi epi) {
+  const int QT = (Q + RX - 1) / RX, PT = (P + RY - 1) / RY;
+  for (int tile = threadIdx.x; tile < PT * QT; tile += blockDim.x) {
+    const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
+    int pi[RY], qj[RX];
+#pragma unroll
+    for (int i = 0; i < RY; ++i) pi[i] = min(p0 + i, P - 1);
+#pragma unroll
+    for (int j = 0; j < RX; ++j) qj[j] = min(q0 + j, Q - 1);
+    R cr[RY][RX], ci[RY][RX];
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j) cr[i][j] = ci[i][j] = R(0);
+#pragma unroll 4
+    for (int k = 0; k < KD; ++k) {
+      R ar[RY], ai[RY], br[RX], bi[RX];
+#pragma unroll
+      for (int i = 0; i < RY; ++i) {
+        const int idx = CONJT ? (k * lda + pi[i]) : (pi[i] * lda + k);
+        ar[i] = Ar[idx];
+        ai[i] = Ai[idx];
+      }
+#pragma unroll
+      for (int j = 0; j < RX; ++j) {
+        br[j] = Br[k * ldb + qj[j]];
+        bi[j] = Bi[k * ldb + qj[j]];
+      }
+#pragma unroll
+      for (int i = 0; i < RY; ++i)
+#pragma unroll
+        for (int j = 0; j < RX; ++j) {
+          if (CONJT) {
+            cr[i][j] = fma(ar[i], br[j], fma(ai[i], bi[j], cr[i][j]));
+            ci[i][j] = fma(ar[i], bi[j], fma(-ai[i], br[j], ci[i][j]));
+          } else {
+            cr[i][j] = fma(ar[i], br[j], fma(-ai[i], bi[j], cr[i][j]));
+            ci[i][j] = fma(ar[i], bi[j], fma(ai[i], br[j], ci[i][j]));
+          }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j)
+        if (p0 + i < P && q0 + j < Q) epi(p0 + i, q0 + j, cr[i][j], ci[i][j]);
+  }
+}
+
+// Per-user Grams  gram[k] = sum_{j < ncols} X[kN+a][j] conj(X[kN+b][j])  (fp64),
+// one warp per user, lanes over columns, full Hermitian N x N stored.
+template <typename R, int NN>
+__device__ __forceinline__ void user_grams(const R* __restrict__ Xr, const R* __restrict__ Xi,
+                                           int ld, int ncols, int K, cd* __restrict__ gram) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < K; k += nw) {
+    double sr[NN][NN], si[NN][NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
+    for (int j = lane; j < ncols; j += 32) {
+      double gr[NN], gi[NN];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        gr[a] = (double)Xr[(k * NN + a) * ld + j];
+        gi[a] = (double)Xi[(k * NN + a) * ld + j];
+      }
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
+          sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
+          if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        sr[a][b] = warp_allsum(sr[a][b]);
+        if (b < a) si[a][b] = warp_allsum(si[a][b]);
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
+          if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
+        }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The solver kernel
+// ---------------------------------------------------------------------------
+template <typename R, int NN, int DD>
+struct Engine {
+  using L_t = Layout<R, NN, DD>;
+
+  // smem views
+  R *Hr, *Hi, *Vr[2], *Vi[2], *Gr[2], *Gi[2];
+  RC<R>*Uf, *Pf, *Df;  // per user N x d, R
+  cd *gram, *ucache, *wcache;
+  double *lndetw, *alpha, *fu, *fw, *fv, *rate, *ustat, *red;
+  L_t L;
+
+  __device__ void bind(unsigned char* smem, int M, int K) {
+    L.init(M, K);
+    R* base = reinterpret_cast<R*>(smem);
+    Hr = base + L.oH;
+    Hi = Hr + L.nH;
+    Vr[0] = base + L.oV0; Vi[0] = Vr[0] + L.nV;
+    Vr[1] = base + L.oV1; Vi[1] = Vr[1] + L.nV;
+    Gr[0] = base + L.oG0; Gi[0] = Gr[0] + L.nG;
+    Gr[1] = base + L.oG1; Gi[1] = Gr[1] + L.nG;
+    Uf = reinterpret_cast<RC<R>*>(base + L.oUPD);
+    Pf = Uf + K * NN * DD;
+    Df = Pf + K * NN * DD;
+    double* d = reinterpret_cast<double*>(smem + L.dbl_off);
+    gram = reinterpret_cast<cd*>(d); d += 2 * K * NN * NN;
+    ucache = reinterpret_cast<cd*>(d); d += 2 * K * NN * DD;
+    wcache = reinterpret_cast<cd*>(d); d += 2 * K * DD * DD;
+    lndetw = d; d += K;
+    alpha = d; d += K;
+    fu = d; d += K;
+    fw = d; d += K;
+    fv = d; d += K;
+    rate = d; d += K;
+    ustat = d; d += K;
+    red = d;
+  }
+
+  // Receiver / weight / gradient-factor update of user k from the Gram in
+  // `gram` and the work G in buffer w (Ĝ).  Writes U/P/D (R) for the Ŷ
+  // phase and the fp64 caches.  Returns a per-user status in ustat[k].
+  __device__ void k1_user(int k, const R* Gwr, const R* Gwi, int ldg, double sigma2, bool weighted,
+                          bool want_f) {
+    cd A[NN][NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) A[a][b] = gram[(k * NN + a) * NN + b];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) A[a][a].r += sigma2;
+    cd Lc[NN][NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) Lc[a][b] = A[a][b];
+    double st = 0.0;
+    if (!chol_lower<NN>(Lc)) st = AMMMSE_STATUS_NONFINITE;
+    // G_kk (N x d) and U = A^{-1} G_kk
+    cd Gkk[NN][DD], U[NN][DD];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int s = 0; s < DD; ++s) {
+        const int idx = (k * NN + a) * ldg + k * DD + s;
+        Gkk[a][s] = cmk((double)Gwr[idx], (double)Gwi[idx]);
+        U[a][s] = Gkk[a][s];
+      }
+    chol_solve<NN, DD>(Lc, U);
+    // T = I - U^H G_kk   (the weight-update argument, solvers.py:242)
+    cd T[DD][DD];
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        cd s = cmk(0.0);
+#pragma unroll
+        for (int a = 0; a < NN; ++a) cfmac(s, U[a][p], Gkk[a][q]);
+        T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
+      }
+    double ak = alpha[k];
+    // MSE matrix E (objective.py:84-105) in Gram form:
+    //   E = I - U^H G_kk - G_kk^H U + U^H A U
+    cd E[DD][DD];
+    if (want_f) {
+      cd AU[NN][DD];
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int s = 0; s < DD; ++s) {
+          cd acc = cmk(0.0);
+#pragma unroll
+          for (int b = 0; b < NN; ++b) cfma(acc, A[a][b], U[b][s]);
+          AU[a][s] = acc;
+        }
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) {
+          cd uau = cmk(0.0);
+#pragma unroll
+          for (int a = 0; a < NN; ++a) cfmac(uau, U[a][p], AU[a][q]);
+          // (I - U^H G)[p][q] = T[p][q];  (G^H U)[p][q] = conj((U^H G)[q][p]) = conj(δ - T[q][p])
+          const cd ghu = cconj(csub(cmk(p == q ? 1.0 : 0.0), T[q][p]));
+          E[p][q] = cadd(csub(T[p][q], ghu), uau);
+        }
+      // f_after_u with the previous W (solvers.py:447)
+      double tr = 0.0;
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) {
+          const cd w = wcache[(k * DD + p) * DD + q];
+          tr += w.r * E[q][p].r - w.i * E[q][p].i;
+        }
+      fu[k] = ak * (tr - lndetw[k]);
+    }
+    // W update or identity (solvers.py:461-464)
+    cd W[DD][DD];
+    double lw = 0.0;
+    if (weighted) {
+      cd Tc[DD][DD], Ti[DD][DD];
+      double nT = 0.0;
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) { Tc[p][q] = T[p][q]; nT += cabs2(T[p][q]); }
+      bool ok = inverse_gj<DD>(Tc, Ti);
+      double nTi = 0.0;
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) nTi += cabs2(Ti[p][q]);
+      // Frobenius condition estimate; >= the 2-norm cond of np.linalg.cond
+      const double cond = sqrt(nT) * sqrt(nTi);
+      if (!ok || !isfinite(cond) || cond > kCondLimit) {
+        if (st == 0.0) st = AMMMSE_STATUS_ILL_CONDITIONED;
+      }
+      // hermitianize (linalg.py:12-14)
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q)
+          W[p][q] = cmk(0.5 * (Ti[p][q].r + Ti[q][p].r), 0.5 * (Ti[p][q].i - Ti[q][p].i));
+      cd LW[DD][DD];
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) LW[p][q] = W[p][q];
+      if (!chol_lower<DD>(LW)) {  // eigvalsh(W)[0] <= 0  (solvers.py:249-252)
+        if (st == 0.0) st = AMMMSE_STATUS_ILL_CONDITIONED;
+        lw = 0.0;
+      } else {
+        lw = chol_lndet<DD>(LW);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) W[p][q] = cmk(p == q ? 1.0 : 0.0);
+    }
+    if (want_f) {
+      double tr = 0.0;
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) tr += W[p][q].r * E[q][p].r - W[p][q].i * E[q][p].i;
+      fw[k] = ak * (tr - lw);
+    }
+    // P = α U W (N x d);  D = -P T = α U W (U^H G_kk - I)  (diagonal block of Ŷ)
+    cd Pm[NN][DD];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        cd acc = cmk(0.0);
+#pragma unroll
+        for (int p = 0; p < DD; ++p) cfma(acc, U[a][p], W[p][q]);
+        Pm[a][q] = cscale(acc, ak);
+      }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        cd acc = cmk(0.0);
+#pragma unroll
+        for (int p = 0; p < DD; ++p) cfma(acc, Pm[a][p], T[p][q]);
+        const int o = (k * NN + a) * DD + q;
+        Df[o] = RC<R>{(R)(-acc.r), (R)(-acc.i)};
+        Pf[o] = RC<R>{(R)Pm[a][q].r, (R)Pm[a][q].i};
+        Uf[o] = RC<R>{(R)U[a][q].r, (R)U[a][q].i};
+        ucache[o] = U[a][q];
+      }
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) wcache[(k * DD + p) * DD + q] = W[p][q];
+    lndetw[k] = lw;
+    ustat[k] = st;
+  }
+
+  // Rate and f_after_v terms of user k from the Gram of G_new.
+  __device__ void wsr_user(int k, const R* Gnr, const R* Gni, int ldg, double sigma2) {
+    cd A[NN][NN], Cv[NN][NN], Gkk[NN][DD];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int s = 0; s < DD; ++s) {
+        const int idx = (k * NN + a) * ldg + k * DD + s;
+        Gkk[a][s] = cmk((double)Gnr[idx], (double)Gni[idx]);
+      }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) {
+        A[a][b] = gram[(k * NN + a) * NN + b];
+        cd own = cmk(0.0);
+#pragma unroll
+        for (int s = 0; s < DD; ++s) own = cadd(own, cmulcb(Gkk[a][s], Gkk[b][s]));
+        Cv[a][b] = csub(A[a][b], own);
+      }
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      A[a][a].r += sigma2;
+      A[a][a].i = 0.0;
+      Cv[a][a].r += sigma2;
+      Cv[a][a].i = 0.0;
+    }
+    // f_after_v with this iteration's U, W at the new precoders (solvers.py:471)
+    cd U[NN][DD];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int s = 0; s < DD; ++s) U[a][s] = ucache[(k * NN + a) * DD + s];
+    double tr = 0.0;
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        cd uhg = cmk(0.0), ghu = cmk(0.0), uau = cmk(0.0);
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          cfmac(uhg, U[a][p], Gkk[a][q]);
+          cfmac(ghu, Gkk[a][p], U[a][q]);
+          cd au = cmk(0.0);
+#pragma unroll
+          for (int b = 0; b < NN; ++b) cfma(au, A[a][b], U[b][q]);
+          cfmac(uau, U[a][p], au);
+        }
+        cd e = csub(csub(uau, uhg), ghu);
+        if (p == q) e.r += 1.0;
+        // accumulate Tr(W E): W[q][p] * E[p][q]
+        const cd w = wcache[(k * DD + q) * DD + p];
+        tr += w.r * e.r - w.i * e.i;
+      }
+    fv[k] = alpha[k] * (tr - lndetw[k]);
+    // rate (objective.py:108-128), clipped at 0
+    double r = 0.0;
+    bool ok1 = chol_lower<NN>(A);
+    bool ok2 = chol_lower<NN>(Cv);
+    if (ok1 && ok2) {
+      r = chol_lndet<NN>(A) - chol_lndet<NN>(Cv);
+      r = r > 0.0 ? r : 0.0;
+      rate[k] = alpha[k] * r;
+      ustat[k] = 0.0;
+    } else {
+      rate[k] = 0.0;
+      ustat[k] = AMMMSE_STATUS_NONFINITE;
+    }
+  }
+
+  // Ŷ in place over the work G: (m, j) pairs, j fastest.
+  __device__ void build_yhat(R* Gwr, R* Gwi, int ldg, int K, int KD) {
+    for (int idx = threadIdx.x; idx < K * KD; idx += blockDim.x) {
+      const int m = idx / KD, j = idx - m * KD;
+      const int b = j / DD, s = j - b * DD;
+      R yr[NN], yi[NN];
+      if (b == m) {
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          const RC<R> v = Df[(m * NN + a) * DD + s];
+          yr[a] = v.r;
+          yi[a] = v.i;
+        }
+      } else {
+        R gr[NN], gi[NN];
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          gr[a] = Gwr[(m * NN + a) * ldg + j];
+          gi[a] = Gwi[(m * NN + a) * ldg + j];
+        }
+        R qr[DD], qi[DD];
+#pragma unroll
+        for (int p = 0; p < DD; ++p) {  // q = U_m^H g
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int a = 0; a < NN; ++a) {
+            const RC<R> u = Uf[(m * NN + a) * DD + p];
+            sr = fma(u.r, gr[a], fma(u.i, gi[a], sr));
+            si = fma(u.r, gi[a], fma(-u.i, gr[a], si));
+          }
+          qr[p] = sr;
+          qi[p] = si;
+        }
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {  // y = P_m q
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int p = 0; p < DD; ++p) {
+            const RC<R> pp = Pf[(m * NN + a) * DD + p];
+            sr = fma(pp.r, qr[p], fma(-pp.i, qi[p], sr));
+            si = fma(pp.r, qi[p], fma(pp.i, qr[p], si));
+          }
+          yr[a] = sr;
+          yi[a] = si;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        Gwr[(m * NN + a) * ldg + j] = yr[a];
+        Gwi[(m * NN + a) * ldg + j] = yi[a];
+      }
+    }
+  }
+
+  // GEMM-B: G[dst] = H · V[src]
+  __device__ void gemm_hv(int src, int dst) {
+    R* gr = Gr[dst];
+    R* gi = Gi[dst];
+    const int ldg = L.ldg;
+    cgemm_smem<R, 2, 2, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
+                               [&](int p, int q, R cr, R ci) {
+                                 gr[p * ldg + q] = cr;
+                                 gi[p * ldg + q] = ci;
+                               });
+  }
+
+  // GEMM-A + projection input: X = V̂ − step · H^H Ŷ into V[dst], returns ‖X‖² (fp64,
+  // block-reduced).  V̂ = Vc + ω (Vc − V[dst]) when extrap, else Vc.
+  __device__ double gemm_grad_step(int ysrc, int vcur, int dst, double step, double omega,
+                                   bool extrap) {
+    const R* vcr = Vr[vcur];
+    const R* vci = Vi[vcur];
+    R* xr = Vr[dst];
+    R* xi = Vi[dst];
+    const int ldv = L.ldv;
+    const R st = (R)step, om = (R)omega;
+    double pw = 0.0;
+    cgemm_smem<R, 2, 2, true>(L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
+                              [&](int p, int q, R gr, R gi) {
+                                const int o = p * ldv + q;
+                                R vr = vcr[o], vi = vci[o];
+                                if (extrap) {  // cur + ω (cur − prev)   (solvers.py:390)
+                                  vr = vr + om * (vr - xr[o]);
+                                  vi = vi + om * (vi - xi[o]);
+                                }
+                                const R x_r = vr - st * gr;
+                                const R x_i = vi - st * gi;
+                                xr[o] = x_r;
+                                xi[o] = x_i;
+                                pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
+                              });
+    return block_sum(pw, red);
+  }
+};
+
+template <typename R, int NN, int DD>
+__global__ void __launch_bounds__(kMaxThreads) ammmse_solve_kernel(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Ctl ctl;
+  __shared__ unsigned long long s_r;
+  Engine<R, NN, DD> e;
+  e.bind(smem, a.M, a.K);
+  const int tid = threadIdx.x;
+  const int M = a.M, K = a.K, KN = K * NN, KD = K * DD;
+  const int ldh = e.L.ldh, ldv = e.L.ldv, ldg = e.L.ldg;
+
+  for (;;) {
+    if (tid == 0) s_r = atomicAdd(a.counter, 1ULL);
+    __syncthreads();
+    const long long r = (long long)s_r;
+    if (r >= a.B) break;
+
+    // ---------------- load realization r ----------------
+    {
+      const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
+      for (int i = tid; i < KN * M; i += blockDim.x) {
+        const int row = i / M, col = i - row * M;
+        const RC<R> v = Hg[i];
+        e.Hr[row * ldh + col] = v.r;
+        e.Hi[row * ldh + col] = v.i;
+      }
+      // V0 (K, M, d) -> V[0] (M x Kd), column k*d+s
+      const RC<R>* Vg = reinterpret_cast<const RC<R>*>(a.V0) + (size_t)r * K * M * DD;
+      for (int i = tid; i < K * M * DD; i += blockDim.x) {
+        const int k = i / (M * DD), rem = i - k * M * DD, m = rem / DD, s = rem - m * DD;
+        const RC<R> v = Vg[i];
+        e.Vr[0][m * ldv + k * DD + s] = v.r;
+        e.Vi[0][m * ldv + k * DD + s] = v.i;
+      }
+      for (int k = tid; k < K; k += blockDim.x) {
+        e.alpha[k] = a.alpha[(size_t)r * K + k];
+        e.lndetw[k] = 0.0;  // W_prev = I at t = 1 (solvers.py:429-430)
+        for (int p = 0; p < DD; ++p)
+          for (int q = 0; q < DD; ++q) e.wcache[(k * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
+      }
+      if (tid == 0) {
+        ctl.sigma2 = a.sigma2[r];
+        ctl.pmax = a.pmax[r];
+        ctl.omega = a.omega;
+        ctl.nhist = 0;
+        ctl.wsr_last = ctl.wsr_prev = 0.0;
+        ctl.running_max = -INFINITY;
+        ctl.drop_streak = 0;
+        ctl.latched = 0;  // start_weighted=False for A-MMMSE (solvers.py:549-550)
+        ctl.switch_it = -1;
+        ctl.weighted_now = 0;
+        ctl.last_weighted = 0;
+        ctl.cur = 0;
+        ctl.stop = 0;
+        ctl.status = 0;
+        ctl.converged = 0;
+        ctl.iters = 0;
+        ctl.f_u = ctl.f_w = ctl.f_v = ctl.wsr = 0.0;
+      }
+    }
+    __syncthreads();
+
+    // ---------------- bounds: kappa, gamma_safe (objective.py:216-240) ----------------
+    user_grams<R, NN>(e.Hr, e.Hi, ldh, M, K, e.gram);
+    __syncthreads();
+    for (int k = tid; k < K; k += blockDim.x) {
+      cd G[NN][NN];
+      for (int p = 0; p < NN; ++p)
+        for (int q = 0; q < NN; ++q) G[p][q] = e.gram[(k * NN + p) * NN + q];
+      e.rate[k] = herm_eig_max<NN>(G);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double kappa = 0.0, abar = e.alpha[0];
+      for (int k = 0; k < K; ++k) {
+        kappa = fmax(kappa, e.rate[k]);
+        abar = fmax(abar, e.alpha[k]);
+      }
+      const double l_v = 2.0 * abar * K * kappa / ctl.sigma2;
+      ctl.gamma_safe = 1.0 / l_v;
+      ctl.gamma = a.gamma_safe ? ctl.gamma_safe : a.gamma;
+      ctl.step = 2.0 * ctl.gamma;
+      if (a.gamma_used) a.gamma_used[r] = ctl.gamma;
+    }
+    // initial G = H V0
+    e.gemm_hv(0, 0);
+    __syncthreads();
+
+    // ---------------- main loop (solvers.py:440-505) ----------------
+    for (int t = 1; t <= a.max_iters; ++t) {
+      const int cur = ctl.cur, oth = 1 - cur;
+      if (tid == 0) {  // stage test (solvers.py:449-459)
+        int wn;
+        if (ctl.latched) {
+          wn = 1;
+        } else {
+          double rs = INFINITY;
+          if (ctl.nhist >= 2) {
+            const double den = fabs(ctl.wsr_prev);
+            rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
+          }
+          wn = rs <= a.eps1;
+          if (wn) {
+            if (a.latch) ctl.latched = 1;
+            if (ctl.switch_it < 0) ctl.switch_it = t;
+          }
+        }
+        ctl.weighted_now = wn;
+      }
+      const bool extrap = (t >= 2) && (ctl.omega > 0.0);
+      // Ĝ into the work buffer (the G_old slot)
+      {
+        const R om = (R)ctl.omega;
+        R *gcr = e.Gr[cur], *gci = e.Gi[cur], *gwr = e.Gr[oth], *gwi = e.Gi[oth];
+        for (int i = tid; i < KN * KD; i += blockDim.x) {
+          const int row = i / KD, col = i - row * KD, o = row * ldg + col;
+          R xr = gcr[o], xi = gci[o];
+          if (extrap) {
+            xr = xr + om * (xr - gwr[o]);
+            xi = xi + om * (xi - gwi[o]);
+          }
+          gwr[o] = xr;
+          gwi[o] = xi;
+        }
+      }
+      __syncthreads();
+      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
+      __syncthreads();
+      const bool weighted = ctl.weighted_now;
+      for (int k = tid; k < K; k += blockDim.x)
+        e.k1_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, weighted, true);
+      __syncthreads();
+      if (tid == 0) {
+        double su = 0.0, sw = 0.0;
+        int st = 0;
+        for (int k = 0; k < K; ++k) {
+          su += e.fu[k];
+          sw += e.fw[k];
+          if (st == 0 && e.ustat[k] != 0.0) st = (int)e.ustat[k];
+        }
+        ctl.f_u = su;
+        ctl.f_w = sw;
+        if (st) {
+          ctl.status = st;
+          ctl.stop = 1;
+        }
+      }
+      __syncthreads();
+      if (ctl.stop) break;
+      e.build_yhat(e.Gr[oth], e.Gi[oth], ldg, K, KD);
+      __syncthreads();
+      // X = V̂ − γ ∇ into V[oth], power
+      const double power = e.gemm_grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
+      const double pmax = ctl.pmax;
+      double scale = 1.0;
+      if (!(power <= pmax)) scale = sqrt(pmax / power);  // project_sum_power (solvers.py:257-263)
+      if (scale != 1.0) {
+        const R sc = (R)scale;
+        R *xr = e.Vr[oth], *xi = e.Vi[oth];
+        for (int i = tid; i < M * KD; i += blockDim.x) {
+          const int row = i / KD, col = i - row * KD, o = row * ldv + col;
+          xr[o] *= sc;
+          xi[o] *= sc;
+        }
+      }
+      __syncthreads();
+      e.gemm_hv(oth, oth);  // G_new = H V_new (Ŷ is dead)
+      __syncthreads();
+      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
+      __syncthreads();
+      for (int k = tid; k < K; k += blockDim.x) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
+      __syncthreads();
+      if (tid == 0) {
+        double wsr = 0.0, sv = 0.0;
+        int st = 0;
+        for (int k = 0; k < K; ++k) {
+          wsr += e.rate[k];
+          sv += e.fv[k];
+          if (st == 0 && e.ustat[k] != 0.0) st = (int)e.ustat[k];
+        }
+        const double total_power = scale == 1.0 ? power : power * scale * scale;
+        if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
+        double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
+        if (t > 1) {
+          const double den = fabs(ctl.wsr_last);
+          rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
+        }
+        ctl.wsr_prev = ctl.wsr_last;
+        ctl.wsr_last = wsr;
+        ctl.nhist += 1;
+        ctl.iters = t;
+        ctl.wsr = wsr;
+        ctl.f_v = sv;
+        ctl.last_weighted = ctl.weighted_now;
+        if (a.trace) {
+          double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
+          tr[AMMMSE_TRACE_T] = (double)t;
+          tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
+          tr[AMMMSE_TRACE_F_VALUE] = sv;
+          tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
+          tr[AMMMSE_TRACE_STAGE] = (double)ctl.weighted_now;
+          tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
+          tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
+          tr[AMMMSE_TRACE_F_AFTER_V] = sv;
+          tr[AMMMSE_TRACE_REL_CHANGE] = rel;
+        }
+        // divergence detector (solvers.py:490-500)
+        ctl.running_max = fmax(ctl.running_max, wsr);
+        if (wsr < 0.5 * ctl.running_max)
+          ctl.drop_streak += 1;
+        else
+          ctl.drop_streak = 0;
+        if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
+        if (st) {
+          ctl.status = st;
+          ctl.stop = 1;
+        } else {
+          ctl.cur = oth;  // shift (solvers.py:502)
+          if (ctl.weighted_now && rel <= a.eps2) {  // stop test (:503-505)
+            ctl.converged = 1;
+            ctl.stop = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (ctl.stop) break;
+    }
+
+    // ---------------- exit: stationarity residual (solvers.py:400-412, :507-509) ----------------
+    double residual = NAN;
+    if (ctl.status == 0) {
+      const int cur = ctl.cur, oth = 1 - cur;
+      const bool weighted = ctl.latched || ctl.last_weighted;
+      for (int i = tid; i < KN * KD; i += blockDim.x) {
+        const int row = i / KD, col = i - row * KD, o = row * ldg + col;
+        e.Gr[oth][o] = e.Gr[cur][o];
+        e.Gi[oth][o] = e.Gi[cur][o];
+      }
+      __syncthreads();
+      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
+      __syncthreads();
+      for (int k = tid; k < K; k += blockDim.x)
+        e.k1_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, weighted, false);
+      __syncthreads();
+      if (tid == 0) {
+        int st = 0;
+        for (int k = 0; k < K; ++k)
+          if (st == 0 && e.ustat[k] != 0.0) st = (int)e.ustat[k];
+        ctl.status = st;
+      }
+      __syncthreads();
+      if (ctl.status == 0) {
+        e.build_yhat(e.Gr[oth], e.Gi[oth], ldg, K, KD);
+        __syncthreads();
+        const double power = e.gemm_grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false);
+        double scale = 1.0;
+        if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
+        double dsum = 0.0, vsum = 0.0;
+        const R* vr = e.Vr[cur];
+        const R* vi = e.Vi[cur];
+        const R* xr = e.Vr[oth];
+        const R* xi = e.Vi[oth];
+        for (int i = tid; i < M * KD; i += blockDim.x) {
+          const int row = i / KD, col = i - row * KD, o = row * ldv + col;
+          const double a_r = (double)vr[o], a_i = (double)vi[o];
+          const double dr = a_r - (double)((R)(xr[o] * (R)scale));
+          const double di = a_i - (double)((R)(xi[o] * (R)scale));
+          dsum += dr * dr + di * di;
+          vsum += a_r * a_r + a_i * a_i;
+        }
+        dsum = block_sum(dsum, e.red);
+        vsum = block_sum(vsum, e.red);
+        residual = sqrt(dsum) / fmax(1.0, sqrt(fmax(vsum, 0.0)));
+      }
+    }
+
+    // ---------------- write results ----------------
+    {
+      const int cur = ctl.cur;
+      if (a.Vout) {
+        RC<R>* Vg = reinterpret_cast<RC<R>*>(a.Vout) + (size_t)r * K * M * DD;
+        for (int i = tid; i < K * M * DD; i += blockDim.x) {
+          const int k = i / (M * DD), rem = i - k * M * DD, m = rem / DD, s = rem - m * DD;
+          Vg[i] = RC<R>{e.Vr[cur][m * ldv + k * DD + s], e.Vi[cur][m * ldv + k * DD + s]};
+        }
+      }
+      if (tid == 0) {
+        if (a.wsr_bits) a.wsr_bits[r] = ctl.wsr / kLn2;
+        if (a.iterations) a.iterations[r] = ctl.iters;
+        if (a.converged) a.converged[r] = (unsigned char)ctl.converged;
+        if (a.residual) a.residual[r] = residual;
+        if (a.switch_it) a.switch_it[r] = ctl.switch_it;
+        if (a.status) a.status[r] = ctl.status;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Standalone bounds kernel: one CTA per realization (objective.py:216-240)
+// ---------------------------------------------------------------------------
+template <typename R, int NN>
+__global__ void __launch_bounds__(128) ammmse_bounds_kernel(const void* H, const double* alpha,
+                                                           const double* pmax,
+                                                           const double* sigma2, int M, int K,
+                                                           long long B, double* out) {
+  __shared__ double lam[1024];
+  const long long r = blockIdx.x;
+  if (r >= B) return;
+  const RC<R>* Hg = reinterpret_cast<const RC<R>*>(H) + (size_t)r * K * NN * M;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < K; k += nw) {
+    double sr[NN][NN], si[NN][NN];
+    for (int p = 0; p < NN; ++p)
+      for (int q = 0; q < NN; ++q) sr[p][q] = si[p][q] = 0.0;
+    for (int m = lane; m < M; m += 32) {
+      double gr[NN], gi[NN];
+      for (int p = 0; p < NN; ++p) {
+        const RC<R> v = Hg[(size_t)(k * NN + p) * M + m];
+        gr[p] = v.r;
+        gi[p] = v.i;
+      }
+      for (int p = 0; p < NN; ++p)
+        for (int q = 0; q < NN; ++q) {
+          sr[p][q] = fma(gr[p], gr[q], fma(gi[p], gi[q], sr[p][q]));
+          si[p][q] = fma(gi[p], gr[q], fma(-gr[p], gi[q], si[p][q]));
+        }
+    }
+    cd G[NN][NN];
+    for (int p = 0; p < NN; ++p)
+      for (int q = 0; q < NN; ++q) G[p][q] = cmk(warp_allsum(sr[p][q]), warp_allsum(si[p][q]));
+    if (lane == 0 && k < 1024) lam[k] = herm_eig_max<NN>(G);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double kappa = 0.0, abar = alpha[(size_t)r * K];
+    for (int k = 0; k < K; ++k) {
+      kappa = fmax(kappa, lam[k]);
+      abar = fmax(abar, alpha[(size_t)r * K + k]);
+    }
+    const double s2 = sigma2[r];
+    const double l_v = 2.0 * abar * K * kappa / s2;
+    double* o = out + (size_t)r * AMMMSE_BOUND_FIELDS;
+    o[AMMMSE_BOUND_KAPPA] = kappa;
+    o[AMMMSE_BOUND_L_V] = l_v;
+    o[AMMMSE_BOUND_GAMMA_SAFE] = 1.0 / l_v;
+    o[AMMMSE_BOUND_EK_FLOOR] = s2 / (pmax[r] * kappa + s2);
+    o[AMMMSE_BOUND_ALPHA_BAR] = abar;
+  }
+}
+
+}  // namespace ammmse

@@ -1,0 +1,23 @@
+// entries.h — table of compiled engine instantiations (one .cu per (R, N)).
+#pragma once
+#include <stddef.h>
+
+namespace ammmse {
+
+struct KernelEntry {
+  const void* solve;                    // ammmse_solve_kernel<R, N, d>
+  const void* bounds;                   // ammmse_bounds_kernel<R, N>
+  size_t (*smem_bytes)(int M, int K);   // Layout<R, N, d>::bytes
+};
+
+// entries_<real>_<N>()[d - 1], d = 1..4
+const KernelEntry* entries_float_1();
+const KernelEntry* entries_float_2();
+const KernelEntry* entries_float_3();
+const KernelEntry* entries_float_4();
+const KernelEntry* entries_double_1();
+const KernelEntry* entries_double_2();
+const KernelEntry* entries_double_3();
+const KernelEntry* entries_double_4();
+
+}  // namespace ammmse

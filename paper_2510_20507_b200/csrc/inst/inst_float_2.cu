@@ -1,0 +1,21 @@
+// Generated instantiation unit: engine kernels for R=float, N=2, d=1..4.
+#include "../ammmse_engine.cuh"
+#include "../entries.h"
+
+namespace ammmse {
+namespace {
+template <int DD>
+size_t smem_fn(int M, int K) {
+  Layout<float, 2, DD> L;
+  L.init(M, K);
+  return L.bytes;
+}
+const KernelEntry kEntries[4] = {
+    {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>},
+    {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>},
+    {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>},
+    {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>},
+};
+}  // namespace
+const KernelEntry* entries_float_2() { return kEntries; }
+}  // namespace ammmse

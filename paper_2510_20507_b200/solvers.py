@@ -1,0 +1,443 @@
+"""Drop-in A-MMMSE driver backed by the B200 engine.
+
+Mirrors the reference solver interface for the A-MMMSE path
+(`pkg/src/wsrbeam/solvers.py`): ``SolverOptions`` (:88-136),
+``IterationRecord`` (:139-156), ``SolveResult`` (:174-182),
+``default_step_parameters`` / ``resolve_step_parameters`` (:185-207),
+``run_ammmse`` (:540-550) and ``solve`` (:560-562) keep their names,
+argument meaning and error behaviour.  The loop itself runs on the GPU
+(libammmse.so) for a whole batch of realizations per call:
+
+  * :func:`run_ammmse`        one realization, reference signature, raises the
+                              reference's exceptions;
+  * :func:`run_ammmse_batch`  B realizations (SoA in, SoA out, per-realization
+                              status codes instead of exceptions, as the
+                              reference harness records them, harness.py:277-278);
+  * :class:`AmmmseEngine`     device-resident entry point (torch tensors in
+                              HBM, stream-ordered) used by the benchmark.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, NativeLibraryError, raise_for_status
+from .model import ChannelSet, PrecoderSet, Stage, SystemConfig, init_precoders, project_sum_power
+
+GAMMA_SAFE = "safe"
+
+#: (omega, gamma) per SNR in dB, paper Table I (ref solvers.py:61-69)
+STEP_DEFAULTS_BY_SNR: dict = {
+    -10.0: (0.6, 0.4),
+    -5.0: (0.6, 0.4),
+    0.0: (0.6, 0.4),
+    5.0: (0.6, 0.4),
+    10.0: (0.8, 0.05),
+    15.0: (0.8, 0.005),
+    20.0: (0.8, 0.003),
+}
+
+
+class Algorithm(Enum):
+    WMMSE = "wmmse"
+    MMMSE = "mmmse"
+    AMMMSE = "ammmse"
+
+    @classmethod
+    def from_name(cls, name: str) -> "Algorithm":
+        key = str(name).strip().lower()
+        for a in cls:
+            if a.value == key:
+                return a
+        raise ConfigError(f"unknown algorithm {name!r}; expected one of {[a.value for a in cls]}")
+
+
+@dataclass(frozen=True)
+class SolverOptions:
+    """Options of one solve (ref solvers.py:88-136, same fields and checks).
+
+    ``bisect_*`` belong to the exact drivers and are accepted but unused by
+    A-MMMSE; ``record_iterates`` is not supported by the device engine.
+    """
+
+    algorithm: Algorithm = Algorithm.WMMSE
+    gamma: float | str | None = None
+    omega: float | None = None
+    eps1: float = 0.1
+    eps2: float = 0.001
+    max_iters: int = 1000
+    bisect_tol: float = 1e-4
+    bisect_max: int = 100
+    record_iterates: bool = False
+    latch_stage: bool = True
+
+    def __post_init__(self) -> None:
+        if not isinstance(self.algorithm, Algorithm):
+            object.__setattr__(self, "algorithm", Algorithm.from_name(self.algorithm))
+        g = self.gamma
+        if isinstance(g, str):
+            if g != GAMMA_SAFE:
+                raise ConfigError(f"gamma must be positive, {GAMMA_SAFE!r}, or None; got {g!r}")
+        elif g is not None:
+            gf = float(g)
+            if not (math.isfinite(gf) and gf > 0):
+                raise ConfigError(f"gamma must be positive, got {g!r}")
+            object.__setattr__(self, "gamma", gf)
+        if self.omega is not None:
+            om = float(self.omega)
+            if not (0.0 <= om < 1.0):
+                raise ConfigError(f"omega must lie in [0, 1), got {self.omega!r}")
+            object.__setattr__(self, "omega", om)
+        if not (self.eps1 > 0):
+            raise ConfigError(f"eps1 must be positive, got {self.eps1!r}")
+        if not (self.eps2 > 0 and math.isfinite(self.eps2)):
+            raise ConfigError(f"eps2 must be positive and finite, got {self.eps2!r}")
+        if self.eps2 > self.eps1:
+            raise ConfigError(f"eps2 ({self.eps2}) must not exceed eps1 ({self.eps1})")
+        if self.max_iters < 1:
+            raise ConfigError("max_iters must be at least 1")
+        if not (self.bisect_tol > 0):
+            raise ConfigError("bisect_tol must be positive")
+        if self.bisect_max < 1:
+            raise ConfigError("bisect_max must be at least 1")
+
+
+@dataclass(frozen=True)
+class IterationRecord:
+    """One completed iteration (ref solvers.py:139-156)."""
+
+    t: int
+    wsr_bits: float
+    f_value: float
+    total_power: float
+    stage: Stage
+    f_after_u: float
+    f_after_w: float
+    f_after_v: float
+    rel_change: float
+
+
+@dataclass(frozen=True, eq=False)
+class SolveResult:
+    """Result of one realization (ref solvers.py:174-182)."""
+
+    final_precoders: PrecoderSet
+    trace: tuple
+    iterations: int
+    converged: bool
+    stationarity_residual: float
+    switch_iteration: int | None = None
+    iterates: tuple | None = None
+
+
+def default_step_parameters(snr_db: float) -> tuple[float, float]:
+    """(omega, gamma) at the nearest tabulated SNR, ties toward the higher SNR
+    (ref solvers.py:185-193)."""
+    snr = float(snr_db)
+    best = None
+    for s in STEP_DEFAULTS_BY_SNR:
+        key = (abs(s - snr), -s)
+        if best is None or key < best[0]:
+            best = (key, s)
+    return STEP_DEFAULTS_BY_SNR[best[1]]
+
+
+def resolve_step_parameters(options: SolverOptions, snr_db: float, bounds=None):
+    """Concrete (gamma, omega) (ref solvers.py:196-207).
+
+    ``gamma == "safe"`` resolves to ``bounds.gamma_safe`` when a bounds object
+    is given, else to the string sentinel (the engine resolves it on device
+    per realization)."""
+    omega_default, gamma_default = default_step_parameters(snr_db)
+    omega = omega_default if options.omega is None else options.omega
+    if options.gamma is None:
+        gamma = gamma_default
+    elif options.gamma == GAMMA_SAFE:
+        gamma = bounds.gamma_safe if bounds is not None else GAMMA_SAFE
+    else:
+        gamma = float(options.gamma)
+    return gamma, omega
+
+
+# ---------------------------------------------------------------------------
+# device engine
+# ---------------------------------------------------------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class BatchResult:
+    """SoA result of a batched solve (device or host arrays).
+
+    Field order follows SolveResult; ``status`` holds AMMMSE_STATUS_* codes
+    (0 ok, 1 IllConditionedWeightError, 2 UnstableParametersError, 3 non-finite)
+    and ``switch_iteration`` uses -1 for None."""
+
+    final_precoders: object
+    wsr_bits: object
+    iterations: object
+    converged: object
+    stationarity_residual: object
+    switch_iteration: object
+    status: object
+    gamma_used: object
+    trace: object = None
+    omega: float = 0.0
+
+    def to_host(self) -> "BatchResult":
+        def h(x):
+            if x is None:
+                return None
+            return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+        return BatchResult(*(h(getattr(self, f)) for f in (
+            "final_precoders", "wsr_bits", "iterations", "converged", "stationarity_residual",
+            "switch_iteration", "status", "gamma_used", "trace")), omega=self.omega)
+
+    def solve_result(self, i: int) -> SolveResult:
+        """Per-realization SolveResult view (needs a host result with a trace)."""
+        h = self if isinstance(self.wsr_bits, np.ndarray) else self.to_host()
+        n = int(h.iterations[i])
+        records = ()
+        if h.trace is not None:
+            rows = h.trace[i, :n]
+            records = tuple(IterationRecord(
+                t=int(row[0]), wsr_bits=float(row[1]), f_value=float(row[2]),
+                total_power=float(row[3]), stage=Stage.WEIGHTED if row[4] > 0.5 else Stage.UNWEIGHTED,
+                f_after_u=float(row[5]), f_after_w=float(row[6]), f_after_v=float(row[7]),
+                rel_change=float(row[8])) for row in rows)
+        sw = int(h.switch_iteration[i])
+        return SolveResult(
+            final_precoders=PrecoderSet(h.final_precoders[i]),
+            trace=records,
+            iterations=n,
+            converged=bool(h.converged[i]),
+            stationarity_residual=float(h.stationarity_residual[i]),
+            switch_iteration=None if sw < 0 else sw,
+        )
+
+
+class AmmmseEngine:
+    """Stream-ordered batched A-MMMSE on one CUDA device.
+
+    Inputs are torch tensors already in HBM: channels (B, K, N, M) and
+    init_precoders (B, K, M, d), both complex64 or both complex128;
+    noise_power, p_max (B,) and weights (B, K) float64.  All outputs are
+    allocated on the same device.  The call is asynchronous on ``stream``
+    (default: torch's current stream)."""
+
+    def __init__(self, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("the A-MMMSE engine needs a CUDA device (no CPU fallback)")
+        self.lib = _native.lib()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._ws = None
+
+    def dims(self, channels, init_precoders) -> _native.AmmmseDims:
+        torch = _torch()
+        if channels.dim() != 4 or init_precoders.dim() != 4:
+            raise ConfigError("channels must be (B, K, N, M) and init_precoders (B, K, M, d)")
+        B, K, N, M = channels.shape
+        if init_precoders.shape[:3] != (B, K, M):
+            raise ConfigError(f"init_precoders shape {tuple(init_precoders.shape)} does not match "
+                              f"channels {tuple(channels.shape)}")
+        if channels.dtype != init_precoders.dtype:
+            raise ConfigError("channels and init_precoders must share a complex dtype")
+        if channels.dtype == torch.complex64:
+            dt = _native.COMPLEX64
+        elif channels.dtype == torch.complex128:
+            dt = _native.COMPLEX128
+        else:
+            raise ConfigError(f"unsupported dtype {channels.dtype}; use complex64 or complex128")
+        return _native.AmmmseDims(B, M, N, K, int(init_precoders.shape[3]), dt)
+
+    def check(self, dims) -> None:
+        rc = self.lib.ammmse_check_dims(dims)
+        if rc != 0:
+            raise ConfigError(f"shape (M={dims.M}, N={dims.N}, K={dims.K}, d={dims.d}) not supported "
+                              f"by the engine: {_native.error_string(rc)}")
+
+    def _workspace(self, nbytes: int):
+        torch = _torch()
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def solve(self, channels, noise_power, p_max, weights, init_precoders, *, gamma, omega,
+              eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
+              out: BatchResult | None = None, stream=None) -> BatchResult:
+        torch = _torch()
+        dims = self.dims(channels, init_precoders)
+        self.check(dims)
+        B = dims.batch
+        dev = channels.device
+        for name, t in (("noise_power", noise_power), ("p_max", p_max), ("weights", weights)):
+            if t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
+                raise ConfigError(f"{name} must be a contiguous float64 tensor on {dev}")
+        if not channels.is_contiguous() or not init_precoders.is_contiguous():
+            raise ConfigError("channels / init_precoders must be contiguous")
+        if out is None:
+            out = BatchResult(
+                final_precoders=torch.empty_like(init_precoders),
+                wsr_bits=torch.empty(B, dtype=torch.float64, device=dev),
+                iterations=torch.empty(B, dtype=torch.int32, device=dev),
+                converged=torch.empty(B, dtype=torch.uint8, device=dev),
+                stationarity_residual=torch.empty(B, dtype=torch.float64, device=dev),
+                switch_iteration=torch.empty(B, dtype=torch.int32, device=dev),
+                status=torch.empty(B, dtype=torch.int32, device=dev),
+                gamma_used=torch.empty(B, dtype=torch.float64, device=dev),
+                trace=(torch.full((B, int(max_iters), _native.TRACE_FIELDS), float("nan"),
+                                  dtype=torch.float64, device=dev) if record_trace else None),
+            )
+        safe = isinstance(gamma, str)
+        if safe and gamma != GAMMA_SAFE:
+            raise ConfigError(f"gamma must be positive or {GAMMA_SAFE!r}")
+        opts = _native.AmmmseOptions(
+            gamma=0.0 if safe else float(gamma), gamma_safe=1 if safe else 0,
+            max_iters=int(max_iters), omega=float(omega), eps1=float(eps1), eps2=float(eps2),
+            latch_stage=1 if latch_stage else 0, reserved=0)
+        prob = _native.AmmmseProblem(channels.data_ptr(), noise_power.data_ptr(), p_max.data_ptr(),
+                                     weights.data_ptr(), init_precoders.data_ptr())
+        ptr = lambda t: None if t is None else t.data_ptr()
+        res = _native.AmmmseResult(
+            ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
+            ptr(out.stationarity_residual), ptr(out.switch_iteration), ptr(out.status),
+            ptr(out.gamma_used), ptr(out.trace))
+        ws_bytes = int(self.lib.ammmse_workspace_size(dims))
+        ws = self._workspace(ws_bytes)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
+                                   ctypes_stream(stream))
+        if rc != 0:
+            if rc == _native.ERR_INVALID:
+                raise ConfigError(_native.error_string(rc))
+            raise NativeLibraryError(f"ammmse_solve failed: {_native.error_string(rc)}")
+        out.omega = float(omega)
+        return out
+
+    def bounds(self, channels, weights, p_max, noise_power, stream=None):
+        """Batched compute_bounds (ref objective.py:216-240): (B, 5) float64
+        [kappa, l_v, gamma_safe, ek_floor, alpha_bar]."""
+        torch = _torch()
+        B, K, N, M = channels.shape
+        dt = _native.COMPLEX64 if channels.dtype == torch.complex64 else _native.COMPLEX128
+        dims = _native.AmmmseDims(B, M, N, K, 1, dt)
+        out = torch.empty((B, _native.BOUND_FIELDS), dtype=torch.float64, device=channels.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(channels.device)
+        rc = self.lib.ammmse_bounds(dims, channels.data_ptr(), weights.data_ptr(), p_max.data_ptr(),
+                                    noise_power.data_ptr(), out.data_ptr(), ctypes_stream(stream))
+        if rc != 0:
+            raise NativeLibraryError(f"ammmse_bounds failed: {_native.error_string(rc)}")
+        return out
+
+
+def ctypes_stream(stream) -> int:
+    return int(stream.cuda_stream)
+
+
+_ENGINES: dict = {}
+
+
+def engine(device=None) -> AmmmseEngine:
+    torch = _torch()
+    key = torch.cuda.current_device() if device is None else torch.device(device).index
+    if key not in _ENGINES:
+        _ENGINES[key] = AmmmseEngine(device)
+    return _ENGINES[key]
+
+
+def _validate_host_inputs(H, sigma2, p_max, weights, V0):
+    if not np.all(np.isfinite(H)):
+        raise ConfigError("channels contains non-finite entries")
+    if not np.all(np.isfinite(V0)):
+        raise ConfigError("precoders contains non-finite entries")
+    if not np.all((sigma2 > 0) & np.isfinite(sigma2)):
+        raise ConfigError("noise_power must be positive")
+    if not np.all((p_max > 0) & np.isfinite(p_max)):
+        raise ConfigError("p_max must be a positive real")
+    if not np.all((weights > 0) & np.isfinite(weights)):
+        raise ConfigError("weights must all be strictly positive")
+
+
+def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, options: SolverOptions,
+                     snr_db: float = 10.0, record_trace: bool = False, device=None) -> BatchResult:
+    """Solve B realizations from host arrays; returns a host BatchResult.
+
+    channels (B, K, N, M), init_precoders (B, K, M, d): complex64 or
+    complex128 numpy arrays (the engine computes in that precision);
+    noise_power, p_max: (B,) or scalars; weights: (B, K) or (K,).
+    ``snr_db`` only feeds the (omega, gamma) table when options leave them unset."""
+    torch = _torch()
+    if options.algorithm is not Algorithm.AMMMSE:
+        raise ConfigError("options.algorithm must be AMMMSE")
+    if options.record_iterates:
+        raise ConfigError("record_iterates is not supported by the batched device engine")
+    H = np.asarray(channels)
+    V0 = np.asarray(init_precoders)
+    if H.ndim != 4 or V0.ndim != 4:
+        raise ConfigError("channels must be (B, K, N, M) and init_precoders (B, K, M, d)")
+    dt = np.complex64 if (H.dtype == np.complex64 and V0.dtype == np.complex64) else np.complex128
+    H = np.array(H, dtype=dt, order="C", copy=True)
+    V0 = np.array(V0, dtype=dt, order="C", copy=True)
+    B, K = H.shape[0], H.shape[1]
+    s2 = np.broadcast_to(np.asarray(noise_power, dtype=np.float64), (B,)).copy()
+    pm = np.broadcast_to(np.asarray(p_max, dtype=np.float64), (B,)).copy()
+    al = np.broadcast_to(np.asarray(weights, dtype=np.float64), (B, K)).copy()
+    _validate_host_inputs(H, s2, pm, al, V0)
+    gamma, omega = resolve_step_parameters(options, snr_db)
+    eng = engine(device)
+    dev = eng.device
+    out = eng.solve(torch.from_numpy(H).to(dev), torch.from_numpy(s2).to(dev),
+                    torch.from_numpy(pm).to(dev), torch.from_numpy(al).to(dev),
+                    torch.from_numpy(V0).to(dev), gamma=gamma, omega=omega, eps1=options.eps1,
+                    eps2=options.eps2, max_iters=options.max_iters, latch_stage=options.latch_stage,
+                    record_trace=record_trace)
+    return out.to_host()
+
+
+def run_ammmse(channels: ChannelSet, config: SystemConfig, options: SolverOptions,
+               init=None) -> SolveResult:
+    """Reference-signature A-MMMSE solve of one realization (ref solvers.py:540-550).
+
+    ``init`` optionally injects V0 (PrecoderSet or array); by default V0 is
+    ``init_precoders(config)`` exactly as the reference draws it
+    (solvers.py:427).  Raises the reference's exceptions for failed solves."""
+    if options.algorithm is not Algorithm.AMMMSE:
+        raise ConfigError("options.algorithm must be AMMMSE")
+    if channels.noise_power is None:
+        raise ConfigError("channels carry no noise power; call compute_noise_power first")
+    if init is None:
+        init = init_precoders(config, project_sum_power)
+    v0 = init.precoders if isinstance(init, PrecoderSet) else np.asarray(init)
+    H = channels.channels
+    if H.shape != (config.K, config.N, config.M):
+        raise ConfigError(f"channels shape {H.shape} does not match config "
+                          f"(K={config.K}, N={config.N}, M={config.M})")
+    dt = np.complex64 if (H.dtype == np.complex64 and v0.dtype == np.complex64) else np.complex128
+    res = run_ammmse_batch(H[None].astype(dt), channels.noise_power, config.p_max,
+                           config.weight_vector[None], v0[None].astype(dt), options,
+                           snr_db=config.snr_db, record_trace=True)
+    raise_for_status(int(res.status[0]), gamma=float(res.gamma_used[0]), omega=res.omega)
+    return res.solve_result(0)
+
+
+def solve(channels: ChannelSet, config: SystemConfig, options: SolverOptions) -> SolveResult:
+    """Dispatch on options.algorithm (ref solvers.py:553-562).  Only A-MMMSE
+    runs on this engine; the exact drivers are out of scope."""
+    if options.algorithm is Algorithm.AMMMSE:
+        return run_ammmse(channels, config, options)
+    raise ConfigError(f"algorithm {options.algorithm.value!r} is not provided by the B200 engine "
+                      "(only A-MMMSE)")
