@@ -8,8 +8,12 @@ SRCS := $(SRC_DIR)/ammmse_capi.cu $(wildcard $(SRC_DIR)/inst/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS := include/ammmse.h $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/entries.h
 LIB := paper_2510_20507_b200/libammmse.so
+PROBE := paper_2510_20507_b200/libammmse_probe.so
 
-all: $(LIB)
+all: $(LIB) $(PROBE)
+
+$(PROBE): $(SRC_DIR)/tools/probe.cu include/ammmse_probe.h
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Iinclude -shared -o $@ $<
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
@@ -19,6 +23,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(PROBE)
 
 .PHONY: all clean

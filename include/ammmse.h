@@ -94,6 +94,11 @@ typedef struct AmmmseProblem {
   const double* p_max;         /* (B,)   P > 0            (SystemConfig.p_max)     */
   const double* weights;       /* (B, K) alpha_k > 0      (SystemConfig.weights)   */
   const void* init_precoders;  /* (B, K, M, d) complex, V0 (init_precoders(), model.py:225-235) */
+  /* Optional per-realization step parameters (B,), NULL = use AmmmseOptions.
+     The reference resolves (gamma, omega) per sweep point (harness.py:466-472);
+     a batch mixing sweep points carries them per realization. */
+  const double* gamma;         /* > 0; overrides options.gamma and options.gamma_safe */
+  const double* omega;         /* [0, 1); overrides options.omega */
 } AmmmseProblem;
 
 /* SolverOptions (solvers.py:88-136) after resolve_step_parameters (:196-207) */

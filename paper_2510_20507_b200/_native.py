@@ -47,7 +47,8 @@ class AmmmseDims(ctypes.Structure):
 class AmmmseProblem(ctypes.Structure):
     _fields_ = [("channels", ctypes.c_void_p), ("noise_power", ctypes.c_void_p),
                 ("p_max", ctypes.c_void_p), ("weights", ctypes.c_void_p),
-                ("init_precoders", ctypes.c_void_p)]
+                ("init_precoders", ctypes.c_void_p), ("gamma", ctypes.c_void_p),
+                ("omega", ctypes.c_void_p)]
 
 
 class AmmmseOptions(ctypes.Structure):

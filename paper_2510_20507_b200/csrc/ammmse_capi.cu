@@ -108,11 +108,11 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     return AMMMSE_ERR_INVALID;
   }
   // SolverOptions checks (solvers.py:112-132)
-  if (!opt->gamma_safe && !(isfinite(opt->gamma) && opt->gamma > 0)) {
+  if (!prob->gamma && !opt->gamma_safe && !(isfinite(opt->gamma) && opt->gamma > 0)) {
     snprintf(g_err, sizeof g_err, "gamma must be positive, got %g", opt->gamma);
     return AMMMSE_ERR_INVALID;
   }
-  if (!(opt->omega >= 0.0 && opt->omega < 1.0)) {
+  if (!prob->omega && !(opt->omega >= 0.0 && opt->omega < 1.0)) {
     snprintf(g_err, sizeof g_err, "omega must lie in [0, 1), got %g", opt->omega);
     return AMMMSE_ERR_INVALID;
   }
@@ -162,6 +162,8 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.pmax = prob->p_max;
   a.alpha = prob->weights;
   a.V0 = prob->init_precoders;
+  a.gamma_arr = prob->gamma;
+  a.omega_arr = prob->omega;
   a.Vout = res->final_precoders;
   a.wsr_bits = res->wsr_bits;
   a.iterations = res->iterations;

@@ -56,6 +56,8 @@ struct EngineArgs {
   const double* pmax;
   const double* alpha;
   const void* V0;
+  const double* gamma_arr;  // optional (B,)
+  const double* omega_arr;  // optional (B,)
   void* Vout;
   double* wsr_bits;
   int* iterations;
@@ -636,7 +638,7 @@ struct Engine {
 };
 
 template <typename R, int NN, int DD>
-__global__ void __launch_bounds__(kMaxThreads) ammmse_solve_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_solve_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
@@ -678,7 +680,7 @@ __global__ void __launch_bounds__(kMaxThreads) ammmse_solve_kernel(EngineArgs a)
       if (tid == 0) {
         ctl.sigma2 = a.sigma2[r];
         ctl.pmax = a.pmax[r];
-        ctl.omega = a.omega;
+        ctl.omega = a.omega_arr ? a.omega_arr[r] : a.omega;
         ctl.nhist = 0;
         ctl.wsr_last = ctl.wsr_prev = 0.0;
         ctl.running_max = -INFINITY;
@@ -715,7 +717,7 @@ __global__ void __launch_bounds__(kMaxThreads) ammmse_solve_kernel(EngineArgs a)
       }
       const double l_v = 2.0 * abar * K * kappa / ctl.sigma2;
       ctl.gamma_safe = 1.0 / l_v;
-      ctl.gamma = a.gamma_safe ? ctl.gamma_safe : a.gamma;
+      ctl.gamma = a.gamma_arr ? a.gamma_arr[r] : (a.gamma_safe ? ctl.gamma_safe : a.gamma);
       ctl.step = 2.0 * ctl.gamma;
       if (a.gamma_used) a.gamma_used[r] = ctl.gamma;
     }

@@ -36,14 +36,23 @@ class Batch:
     p_max: np.ndarray           # (B,) float64
     weights: np.ndarray         # (B, K) float64
     init_precoders: np.ndarray  # (B, K, M, d) complex
+    gamma: np.ndarray | None = None  # (B,) per-realization step (optional)
+    omega: np.ndarray | None = None  # (B,) per-realization extrapolation (optional)
 
     @property
     def B(self) -> int:
         return self.channels.shape[0]
 
     def subset(self, idx) -> "Batch":
+        sel = lambda a: None if a is None else a[idx]
         return Batch(self.channels[idx], self.noise_power[idx], self.p_max[idx], self.weights[idx],
-                     self.init_precoders[idx])
+                     self.init_precoders[idx], sel(self.gamma), sel(self.omega))
+
+    @staticmethod
+    def concat(parts) -> "Batch":
+        cat = lambda f: np.concatenate([getattr(p, f) for p in parts])
+        return Batch(cat("channels"), cat("noise_power"), cat("p_max"), cat("weights"),
+                     cat("init_precoders"), cat("gamma"), cat("omega"))
 
 
 def uniform_weights(r: int, K: int) -> np.ndarray:
@@ -106,9 +115,12 @@ class Workload:
     snr_db: float = 20.0
 
     def batch(self, B: int | None = None, seed0: int = 0) -> Batch:
-        return build_batch(self.M, self.N, self.K, self.d, self.B if B is None else B,
-                           p_max=self.p_max, weights=self.weights, channel=self.channel,
-                           dtype=self.dtype, seed0=seed0)
+        b = build_batch(self.M, self.N, self.K, self.d, self.B if B is None else B,
+                        p_max=self.p_max, weights=self.weights, channel=self.channel,
+                        dtype=self.dtype, seed0=seed0)
+        b.gamma = np.full(b.B, self.gamma)
+        b.omega = np.full(b.B, self.omega)
+        return b
 
 
 TINY = np.finfo(np.float64).tiny * np.finfo(np.float64).eps  # smallest positive double (5e-324)
@@ -116,25 +128,25 @@ TINY = np.finfo(np.float64).tiny * np.finfo(np.float64).eps  # smallest positive
 WORKLOADS = {
     # [0] small CPU-oracle case, complex128
     "small": Workload("small", 16, 2, 4, 2, 64, 100.0, "ones", "iid", np.complex128,
-                      1e-6, 200, gamma=0.01, omega=0.8, snr_db=20.0),
+                      1e-6, 200, gamma=0.016, omega=0.8, snr_db=20.0),
     # [1] medium case, one entry per SNR point of the sweep {0,10,20,30} dB
     "medium_snr0": Workload("medium_snr0", 64, 2, 16, 2, 4096, 1.0, "uniform", "iid",
-                            np.complex64, 1e-5, 300, gamma=0.004, omega=0.8, snr_db=0.0),
+                            np.complex64, 1e-5, 300, gamma=0.001, omega=0.8, snr_db=0.0),
     "medium_snr10": Workload("medium_snr10", 64, 2, 16, 2, 4096, 10.0, "uniform", "iid",
                              np.complex64, 1e-5, 300, gamma=0.004, omega=0.8, snr_db=10.0),
     "medium_snr20": Workload("medium_snr20", 64, 2, 16, 2, 4096, 100.0, "uniform", "iid",
-                             np.complex64, 1e-5, 300, gamma=0.004, omega=0.8, snr_db=20.0),
+                             np.complex64, 1e-5, 300, gamma=0.002, omega=0.8, snr_db=20.0),
     "medium_snr30": Workload("medium_snr30", 64, 2, 16, 2, 4096, 1000.0, "uniform", "iid",
-                             np.complex64, 1e-5, 300, gamma=0.004, omega=0.8, snr_db=30.0),
+                             np.complex64, 1e-5, 300, gamma=0.002, omega=0.8, snr_db=30.0),
     # [2] large-array case
     "large": Workload("large", 128, 4, 32, 4, 8192, 100.0, "uniform", "iid", np.complex64,
-                      1e-5, 500, gamma=0.001, omega=0.8, snr_db=20.0),
+                      1e-5, 500, gamma=0.002, omega=0.8, snr_db=20.0),
     # [3] massive MIMO, Kronecker-correlated
     "massive": Workload("massive", 256, 2, 64, 2, 16384, 100.0, "ones", "kronecker",
                         np.complex64, 1e-5, 500, gamma=0.001, omega=0.8, snr_db=20.0),
 }
 # [4] throughput sweep: exactly 50 iterations (eps2 = smallest positive double)
-for _M, _g in ((32, 0.01), (64, 0.004), (128, 0.002), (256, 0.001), (512, 0.0005)):
+for _M, _g in ((32, 0.008), (64, 0.004), (128, 0.002), (256, 0.001), (512, 0.0005)):
     WORKLOADS[f"sweep{_M}"] = Workload(f"sweep{_M}", _M, 2, _M // 4, 2, 65536, 10 ** 1.5, "uniform",
                                        "iid", np.complex64, TINY, 50, gamma=_g, omega=0.8,
                                        snr_db=15.0)

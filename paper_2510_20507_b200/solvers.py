@@ -300,15 +300,24 @@ class AmmmseEngine:
                 trace=(torch.full((B, int(max_iters), _native.TRACE_FIELDS), float("nan"),
                                   dtype=torch.float64, device=dev) if record_trace else None),
             )
-        safe = isinstance(gamma, str)
+        # gamma: float | "safe" | (B,) float64 tensor;  omega: float | (B,) float64 tensor
+        g_arr = gamma if torch.is_tensor(gamma) else None
+        o_arr = omega if torch.is_tensor(omega) else None
+        for name, t in (("gamma", g_arr), ("omega", o_arr)):
+            if t is not None and (t.dtype != torch.float64 or t.device != dev or t.shape != (B,)
+                                  or not t.is_contiguous()):
+                raise ConfigError(f"per-realization {name} must be a contiguous ({B},) float64 tensor on {dev}")
+        safe = g_arr is None and isinstance(gamma, str)
         if safe and gamma != GAMMA_SAFE:
             raise ConfigError(f"gamma must be positive or {GAMMA_SAFE!r}")
         opts = _native.AmmmseOptions(
-            gamma=0.0 if safe else float(gamma), gamma_safe=1 if safe else 0,
-            max_iters=int(max_iters), omega=float(omega), eps1=float(eps1), eps2=float(eps2),
-            latch_stage=1 if latch_stage else 0, reserved=0)
+            gamma=0.0 if (safe or g_arr is not None) else float(gamma), gamma_safe=1 if safe else 0,
+            max_iters=int(max_iters), omega=0.0 if o_arr is not None else float(omega),
+            eps1=float(eps1), eps2=float(eps2), latch_stage=1 if latch_stage else 0, reserved=0)
         prob = _native.AmmmseProblem(channels.data_ptr(), noise_power.data_ptr(), p_max.data_ptr(),
-                                     weights.data_ptr(), init_precoders.data_ptr())
+                                     weights.data_ptr(), init_precoders.data_ptr(),
+                                     None if g_arr is None else g_arr.data_ptr(),
+                                     None if o_arr is None else o_arr.data_ptr())
         ptr = lambda t: None if t is None else t.data_ptr()
         res = _native.AmmmseResult(
             ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
@@ -324,7 +333,7 @@ class AmmmseEngine:
             if rc == _native.ERR_INVALID:
                 raise ConfigError(_native.error_string(rc))
             raise NativeLibraryError(f"ammmse_solve failed: {_native.error_string(rc)}")
-        out.omega = float(omega)
+        out.omega = omega if o_arr is None else o_arr
         return out
 
     def bounds(self, channels, weights, p_max, noise_power, stream=None):
@@ -353,6 +362,8 @@ _ENGINES: dict = {}
 
 def engine(device=None) -> AmmmseEngine:
     torch = _torch()
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("the A-MMMSE engine needs a CUDA device (no CPU fallback)")
     key = torch.cuda.current_device() if device is None else torch.device(device).index
     if key not in _ENGINES:
         _ENGINES[key] = AmmmseEngine(device)
@@ -373,13 +384,17 @@ def _validate_host_inputs(H, sigma2, p_max, weights, V0):
 
 
 def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, options: SolverOptions,
-                     snr_db: float = 10.0, record_trace: bool = False, device=None) -> BatchResult:
+                     snr_db: float = 10.0, record_trace: bool = False, device=None,
+                     step_gamma=None, step_omega=None) -> BatchResult:
     """Solve B realizations from host arrays; returns a host BatchResult.
 
     channels (B, K, N, M), init_precoders (B, K, M, d): complex64 or
     complex128 numpy arrays (the engine computes in that precision);
     noise_power, p_max: (B,) or scalars; weights: (B, K) or (K,).
-    ``snr_db`` only feeds the (omega, gamma) table when options leave them unset."""
+    ``snr_db`` only feeds the (omega, gamma) table when options leave them unset;
+    ``step_gamma`` / ``step_omega`` ((B,) arrays) override the options per
+    realization, the way the harness resolves them per sweep point
+    (harness.py:466-472)."""
     torch = _torch()
     if options.algorithm is not Algorithm.AMMMSE:
         raise ConfigError("options.algorithm must be AMMMSE")
@@ -400,6 +415,16 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
     gamma, omega = resolve_step_parameters(options, snr_db)
     eng = engine(device)
     dev = eng.device
+    if step_gamma is not None:
+        g = np.broadcast_to(np.asarray(step_gamma, dtype=np.float64), (B,)).copy()
+        if not np.all((g > 0) & np.isfinite(g)):
+            raise ConfigError("gamma must be positive")
+        gamma = torch.from_numpy(g).to(dev)
+    if step_omega is not None:
+        o = np.broadcast_to(np.asarray(step_omega, dtype=np.float64), (B,)).copy()
+        if not np.all((o >= 0) & (o < 1)):
+            raise ConfigError("omega must lie in [0, 1)")
+        omega = torch.from_numpy(o).to(dev)
     out = eng.solve(torch.from_numpy(H).to(dev), torch.from_numpy(s2).to(dev),
                     torch.from_numpy(pm).to(dev), torch.from_numpy(al).to(dev),
                     torch.from_numpy(V0).to(dev), gamma=gamma, omega=omega, eps1=options.eps1,
