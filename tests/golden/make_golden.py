@@ -76,8 +76,9 @@ def cases():
     b = build_batch(16, 2, 4, 2, 3, p_max=10.0, dtype=np.complex128, seed0=11)
     out.append(_case("edge_unlatched", b, dict(gamma=0.01, omega=0.6, eps2=1e-4, max_iters=300,
                                                latch_stage=False)))
-    out.append(_case("edge_table_snr10", b, dict(gamma=None, omega=None, eps2=1e-4, max_iters=300),
-                     snr_db=10.0, note="Table I defaults at 10 dB (0.8, 0.05)"))
+    # Table I at 10 dB (0.05) is chaotic at sigma^2 = 1; 20 dB is not
+    out.append(_case("edge_table_snr20", b, dict(gamma=None, omega=None, eps2=1e-4, max_iters=300),
+                     snr_db=20.0, note="Table I defaults at 20 dB (0.8, 0.003)"))
     out.append(_case("edge_switch_eq_stop", b, dict(gamma=0.01, omega=0.6, eps1=1e-3, eps2=1e-3,
                                                     max_iters=500),
                      note="eps1 == eps2 (test_solvers.py:361-382 analogue)"))
