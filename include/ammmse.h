@@ -110,7 +110,9 @@ typedef struct AmmmseOptions {
   double eps1;         /* stage-switch threshold, > 0, may be +inf                     */
   double eps2;         /* stop threshold, > 0, finite, <= eps1                         */
   int32_t latch_stage; /* 1: latch the weighted stage (default); 0: re-test every iteration */
-  int32_t reserved;
+  int32_t cluster_size;/* 0: automatic engine choice.  c >= 1: force the thread-block-cluster
+                          engine with c CTAs per realization (c in {1,2,4,8,16}, c | K) —
+                          a tuning / testing knob, results are identical up to rounding */
 } AmmmseOptions;
 
 /* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */

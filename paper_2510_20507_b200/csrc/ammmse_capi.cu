@@ -54,6 +54,50 @@ int max_smem_optin() {
   return v;
 }
 
+// Engine choice: one CTA per realization when its state fits one SM's shared
+// memory, else the smallest thread-block cluster (C | K) whose per-CTA slice
+// fits.  force_c >= 1 forces the cluster engine with that many CTAs.
+struct Plan {
+  const ammmse::KernelEntry* e;
+  int cluster;  // 0: single-CTA engine; >= 1: cluster engine with that many CTAs
+  size_t smem;
+  int threads;
+};
+
+int pick_threads(const AmmmseDims* d);
+
+int make_plan(const AmmmseDims* d, int force_c, Plan* p) {
+  const ammmse::KernelEntry* e = lookup(d);
+  if (!e) return AMMMSE_ERR_UNSUPPORTED;
+  int lim = max_smem_optin();
+  if (lim <= 0) lim = 232448;  // sm_100 opt-in limit (no device to query)
+  p->e = e;
+  if (force_c == 0) {
+    const size_t s1 = e->smem_bytes(d->M, d->K);
+    if (s1 <= (size_t)lim) {
+      p->cluster = 0;
+      p->smem = s1;
+      p->threads = pick_threads(d);
+      return AMMMSE_OK;
+    }
+  }
+  const int cands[5] = {1, 2, 4, 8, 16};
+  for (int i = 0; i < 5; ++i) {
+    const int c = cands[i];
+    if (force_c && c != force_c) continue;
+    if (!force_c && c == 1) continue;
+    if (d->K % c) continue;
+    const size_t s = e->cluster_smem_bytes(d->M, d->K, c);
+    if (s <= (size_t)lim) {
+      p->cluster = c;
+      p->smem = s;
+      p->threads = 256;
+      return AMMMSE_OK;
+    }
+  }
+  return AMMMSE_ERR_UNSUPPORTED;
+}
+
 // Threads per CTA: about one 2x2 output tile of the larger GEMM per thread,
 // 64..256, multiple of 32.
 int pick_threads(const AmmmseDims* d) {
@@ -80,14 +124,8 @@ int ammmse_abi_version(void) { return AMMMSE_ABI_VERSION; }
 int ammmse_check_dims(const AmmmseDims* dims) {
   int rc = dims_valid(dims);
   if (rc) return rc;
-  const ammmse::KernelEntry* e = lookup(dims);
-  if (!e) return AMMMSE_ERR_UNSUPPORTED;
-  const size_t need = e->smem_bytes(dims->M, dims->K);
-  // 227 KB is the sm_100 opt-in limit; without a device we cannot query it.
-  int lim = max_smem_optin();
-  if (lim <= 0) lim = 232448;
-  if (need > (size_t)lim) return AMMMSE_ERR_UNSUPPORTED;
-  return AMMMSE_OK;
+  Plan p;
+  return make_plan(dims, 0, &p);
 }
 
 size_t ammmse_workspace_size(const AmmmseDims* dims) {
@@ -132,25 +170,61 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     snprintf(g_err, sizeof g_err, "workspace missing or too small");
     return AMMMSE_ERR_WORKSPACE;
   }
-  const ammmse::KernelEntry* e = lookup(dims);
-  const size_t smem = e->smem_bytes(dims->M, dims->K);
-  const int threads = pick_threads(dims);
-  cudaStream_t s = (cudaStream_t)stream;
-
-  cudaError_t ce = cudaFuncSetAttribute(e->solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaFuncSetAttribute");
-  int per_sm = 0;
-  ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->solve, threads, smem);
-  if (ce != cudaSuccess) return cuda_fail(ce, "occupancy");
-  if (per_sm < 1) {
-    snprintf(g_err, sizeof g_err, "kernel does not fit on an SM (smem %zu)", smem);
+  Plan plan;
+  if (opt->cluster_size < 0 || make_plan(dims, opt->cluster_size, &plan) != AMMMSE_OK) {
+    snprintf(g_err, sizeof g_err, "no engine configuration fits (cluster_size %d)", opt->cluster_size);
     return AMMMSE_ERR_UNSUPPORTED;
   }
+  const void* func = plan.cluster ? plan.e->cluster_solve : plan.e->solve;
+  const size_t smem = plan.smem;
+  const int threads = plan.threads;
+  cudaStream_t s = (cudaStream_t)stream;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  long long grid = (long long)sms * per_sm;
-  if (grid > dims->batch) grid = dims->batch;
+
+  cudaError_t ce = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaFuncSetAttribute");
+  long long grid = 0;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cudaLaunchAttribute attr[1];
+  if (plan.cluster) {
+    if (plan.cluster > 8) {
+      ce = cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (ce != cudaSuccess) return cuda_fail(ce, "non-portable cluster size");
+    }
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)plan.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.gridDim = dim3((unsigned)(plan.cluster * sms));
+    int nclusters = 0;
+    ce = cudaOccupancyMaxActiveClusters(&nclusters, func, &cfg);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaOccupancyMaxActiveClusters");
+    if (nclusters < 1) {
+      snprintf(g_err, sizeof g_err, "cluster of %d CTAs with %zu B smem cannot be resident", plan.cluster, smem);
+      return AMMMSE_ERR_UNSUPPORTED;
+    }
+    long long nc = nclusters < dims->batch ? nclusters : dims->batch;
+    grid = nc * plan.cluster;
+    cfg.gridDim = dim3((unsigned)grid);
+  } else {
+    int per_sm = 0;
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+    if (ce != cudaSuccess) return cuda_fail(ce, "occupancy");
+    if (per_sm < 1) {
+      snprintf(g_err, sizeof g_err, "kernel does not fit on an SM (smem %zu)", smem);
+      return AMMMSE_ERR_UNSUPPORTED;
+    }
+    grid = (long long)sms * per_sm;
+    if (grid > dims->batch) grid = dims->batch;
+  }
 
   ce = cudaMemsetAsync(workspace, 0, 8, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
@@ -185,8 +259,11 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.B = dims->batch;
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
   void* args[] = {&a};
-  ce = cudaLaunchKernel(e->solve, dim3((unsigned)grid), dim3(threads), args, smem, s);
-  if (ce != cudaSuccess) return cuda_fail(ce, "cudaLaunchKernel(solve)");
+  if (plan.cluster)
+    ce = cudaLaunchKernelExC(&cfg, func, args);
+  else
+    ce = cudaLaunchKernel(func, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "kernel launch (solve)");
   return AMMMSE_OK;
 }
 

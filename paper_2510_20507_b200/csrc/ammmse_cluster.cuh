@@ -1,0 +1,625 @@
+// ammmse_cluster.cuh — A-MMMSE engine for realizations whose state does not
+// fit one SM (BASELINE configs 2-4, sweep M >= 128): one thread-block
+// CLUSTER of C CTAs per realization.
+//
+// Partition: CTA c owns users [c*K/C, (c+1)*K/C), i.e. the matching columns
+// of V (M x Kd) and G (KN x Kd).  H (KN x M) is replicated in every CTA's
+// shared memory.  Both GEMMs then need only local columns:
+//     G[:, own] = H V[:, own]          ∇[:, own] = H^H Ŷ[:, own]
+// and the only cross-CTA traffic per iteration is O(K N^2) through
+// distributed shared memory (DSMEM):
+//   * per-user N x N Gram partials  sum_{j in own cols} G_kj G_kj^H  (fp64),
+//     summed by the user's owner in fixed rank order;
+//   * the owners' U_k, α_k U_k W_k (needed by every column block of Ŷ);
+//   * per-CTA scalar partials (objective terms, ‖X‖², rates, status),
+//     summed by every CTA in fixed rank order, so all CTAs take bit-identical
+//     stage / stop / divergence decisions without a broadcast.
+// Five cluster barriers per iteration.  Reference semantics are those of
+// ammmse_engine.cuh (solvers.py:415-518); the per-user math is shared
+// (user_algebra.cuh).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "ammmse_engine.cuh"
+
+namespace ammmse {
+
+namespace cg = cooperative_groups;
+
+// exchange-scalar slots (per CTA, read by every CTA of the cluster)
+enum XSlot {
+  XS_FU = 0, XS_FW, XS_ST1, XS_POWER, XS_RATE, XS_FV, XS_ST2, XS_KAPPA, XS_DSUM, XS_VSUM,
+  XS_ST3, XS_COUNT
+};
+
+template <typename R, int NN, int DD>
+struct CLayout {
+  int M, K, C, KL, KN, KD, ncol, ldh, ldv, ldg;
+  size_t nH, nV, nG;
+  size_t oH, oV0, oV1, oG0, oG1, oUall, oPall, oDown;  // R offsets (planar / RC)
+  size_t dbl_off, bytes;
+
+  __host__ __device__ void init(int M_, int K_, int C_) {
+    M = M_;
+    K = K_;
+    C = C_;
+    KL = K / C;
+    KN = K * NN;
+    KD = K * DD;
+    ncol = KL * DD;
+    ldh = M | 1;
+    ldv = ncol;
+    ldg = ncol;
+    nH = (size_t)KN * ldh;
+    nV = (size_t)M * ldv;
+    nG = (size_t)KN * ldg;
+    oH = 0;
+    oV0 = oH + 2 * nH;
+    oV1 = oV0 + 2 * nV;
+    oG0 = oV1 + 2 * nV;
+    oG1 = oG0 + 2 * nG;
+    oUall = oG1 + 2 * nG;                       // RC<R>[K*NN*DD]
+    oPall = oUall + (size_t)2 * K * NN * DD;
+    oDown = oPall + (size_t)2 * K * NN * DD;    // RC<R>[KL*NN*DD]
+    const size_t nR = oDown + (size_t)2 * KL * NN * DD;
+    dbl_off = ((nR * sizeof(R)) + 15) & ~(size_t)15;
+    bytes = dbl_off + dbl_count() * sizeof(double);
+  }
+  // fp64 region: gx[2] (K*NN*NN cd each), ucache (KL*NN*DD cd), wcache
+  // (KL*DD*DD cd), lndetw, alpha_own, fu, fw, fv, rate, ust (KL each),
+  // xs (XS_COUNT), red (32)
+  __host__ __device__ size_t dbl_count() const {
+    return (size_t)2 * 2 * K * NN * NN + 2 * KL * NN * DD + 2 * KL * DD * DD + 7 * KL + XS_COUNT +
+           32;
+  }
+};
+
+template <typename R, int NN, int DD>
+__global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Ctl ctl;
+  __shared__ unsigned long long s_r;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int C = (int)cl.num_blocks();
+  const int tid = threadIdx.x;
+
+  CLayout<R, NN, DD> L;
+  L.init(a.M, a.K, C);
+  const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
+  const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
+  const int k0 = crank * KL;       // first own user
+  const int col0 = crank * ncol;   // first own global column
+
+  R* base = reinterpret_cast<R*>(smem);
+  R* Hr = base + L.oH;
+  R* Hi = Hr + L.nH;
+  R *Vr[2], *Vi[2], *Gr[2], *Gi[2];
+  Vr[0] = base + L.oV0; Vi[0] = Vr[0] + L.nV;
+  Vr[1] = base + L.oV1; Vi[1] = Vr[1] + L.nV;
+  Gr[0] = base + L.oG0; Gi[0] = Gr[0] + L.nG;
+  Gr[1] = base + L.oG1; Gi[1] = Gr[1] + L.nG;
+  RC<R>* Uall = reinterpret_cast<RC<R>*>(base + L.oUall);
+  RC<R>* Pall = reinterpret_cast<RC<R>*>(base + L.oPall);
+  RC<R>* Down = reinterpret_cast<RC<R>*>(base + L.oDown);
+  double* dp = reinterpret_cast<double*>(smem + L.dbl_off);
+  cd* gx[2];
+  gx[0] = reinterpret_cast<cd*>(dp); dp += 2 * K * NN * NN;
+  gx[1] = reinterpret_cast<cd*>(dp); dp += 2 * K * NN * NN;
+  cd* ucache = reinterpret_cast<cd*>(dp); dp += 2 * KL * NN * DD;
+  cd* wcache = reinterpret_cast<cd*>(dp); dp += 2 * KL * DD * DD;
+  double* lndetw = dp; dp += KL;
+  double* alpha = dp; dp += KL;
+  double* fu = dp; dp += KL;
+  double* fw = dp; dp += KL;
+  double* fv = dp; dp += KL;
+  double* rate = dp; dp += KL;
+  double* ust = dp; dp += KL;
+  double* xs = dp; dp += XS_COUNT;
+  double* red = dp;
+
+  // fixed-order cluster sum / first-nonzero of an exchange slot
+  auto xsum = [&](int slot) {
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += cl.map_shared_rank(xs, c)[slot];
+    return s;
+  };
+  auto xfirst = [&](int slot) {
+    for (int c = 0; c < C; ++c) {
+      const double v = cl.map_shared_rank(xs, c)[slot];
+      if (v != 0.0) return (int)v;
+    }
+    return 0;
+  };
+  // partial Grams over own columns for ALL users: gx[buf][k] (warp per user)
+  auto gram_partials = [&](const R* Xr, const R* Xi, int buf) {
+    user_grams<R, NN>(Xr, Xi, ldg, ncol, K, gx[buf]);
+  };
+  // reduced Gram of own user kl (fixed rank order)
+  auto gram_of = [&](int buf, int kl, cd (&Tg)[NN][NN]) {
+    const int k = k0 + kl;
+#pragma unroll
+    for (int p = 0; p < NN; ++p)
+#pragma unroll
+      for (int q = 0; q < NN; ++q) Tg[p][q] = cmk(0.0);
+    for (int c = 0; c < C; ++c) {
+      const cd* g = cl.map_shared_rank(gx[buf], c) + (size_t)k * NN * NN;
+#pragma unroll
+      for (int p = 0; p < NN; ++p)
+#pragma unroll
+        for (int q = 0; q < NN; ++q) Tg[p][q] = cadd(Tg[p][q], g[p * NN + q]);
+    }
+  };
+  // one pass of per-user K1 for the own users + U/P publication
+  auto k1_phase = [&](int gsrc, bool weighted, bool want_f) {
+    for (int kl = tid; kl < KL; kl += blockDim.x) {
+      cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
+      gram_of(0, kl, Tg);
+#pragma unroll
+      for (int p = 0; p < NN; ++p)
+#pragma unroll
+        for (int s = 0; s < DD; ++s) {
+          const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
+          Gkk[p][s] = cmk((double)Gr[gsrc][idx], (double)Gi[gsrc][idx]);
+        }
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) Wp[p][q] = wcache[(kl * DD + p) * DD + q];
+      K1Out<NN, DD> o;
+      k1_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], Wp, lndetw[kl], weighted, want_f, o);
+#pragma unroll
+      for (int p = 0; p < NN; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) {
+          const int ig = ((k0 + kl) * NN + p) * DD + q, il = (kl * NN + p) * DD + q;
+          Uall[ig] = RC<R>{(R)o.U[p][q].r, (R)o.U[p][q].i};
+          Pall[ig] = RC<R>{(R)o.P[p][q].r, (R)o.P[p][q].i};
+          Down[il] = RC<R>{(R)o.D[p][q].r, (R)o.D[p][q].i};
+          ucache[il] = o.U[p][q];
+        }
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = o.W[p][q];
+      lndetw[kl] = o.lndetw;
+      fu[kl] = o.fu;
+      fw[kl] = o.fw;
+      ust[kl] = o.status;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double su = 0.0, sw = 0.0;
+      int st = 0;
+      for (int kl = 0; kl < KL; ++kl) {
+        su += fu[kl];
+        sw += fw[kl];
+        if (st == 0 && ust[kl] != 0.0) st = (int)ust[kl];
+      }
+      xs[XS_FU] = su;
+      xs[XS_FW] = sw;
+      xs[XS_ST1] = st;
+    }
+    cl.sync();
+    // gather the other owners' U and α U W
+    const int per = NN * DD;
+    for (int i = tid; i < K * per; i += blockDim.x) {
+      const int owner = (i / per) / KL;
+      if (owner != crank) {
+        Uall[i] = cl.map_shared_rank(Uall, owner)[i];
+        Pall[i] = cl.map_shared_rank(Pall, owner)[i];
+      }
+    }
+  };
+  // Ŷ over own columns, in place over G[g]
+  auto build_yhat = [&](int g) {
+    R* Yr = Gr[g];
+    R* Yi = Gi[g];
+    for (int idx = tid; idx < K * ncol; idx += blockDim.x) {
+      const int m = idx / ncol, jl = idx - m * ncol;
+      const int j = col0 + jl, b = j / DD, s = j - b * DD;
+      R yr[NN], yi[NN];
+      if (b == m) {
+#pragma unroll
+        for (int p = 0; p < NN; ++p) {
+          const RC<R> v = Down[((m - k0) * NN + p) * DD + s];
+          yr[p] = v.r;
+          yi[p] = v.i;
+        }
+      } else {
+        R gr[NN], gi[NN], qr[DD], qi[DD];
+#pragma unroll
+        for (int p = 0; p < NN; ++p) {
+          gr[p] = Yr[(m * NN + p) * ldg + jl];
+          gi[p] = Yi[(m * NN + p) * ldg + jl];
+        }
+#pragma unroll
+        for (int q = 0; q < DD; ++q) {
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int p = 0; p < NN; ++p) {
+            const RC<R> u = Uall[(m * NN + p) * DD + q];
+            sr = fma(u.r, gr[p], fma(u.i, gi[p], sr));
+            si = fma(u.r, gi[p], fma(-u.i, gr[p], si));
+          }
+          qr[q] = sr;
+          qi[q] = si;
+        }
+#pragma unroll
+        for (int p = 0; p < NN; ++p) {
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int q = 0; q < DD; ++q) {
+            const RC<R> pp = Pall[(m * NN + p) * DD + q];
+            sr = fma(pp.r, qr[q], fma(-pp.i, qi[q], sr));
+            si = fma(pp.r, qi[q], fma(pp.i, qr[q], si));
+          }
+          yr[p] = sr;
+          yi[p] = si;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NN; ++p) {
+        Yr[(m * NN + p) * ldg + jl] = yr[p];
+        Yi[(m * NN + p) * ldg + jl] = yi[p];
+      }
+    }
+  };
+  // GEMM-A + extrapolation + step, returns cluster-wide ‖X‖²
+  auto grad_step = [&](int ysrc, int vcur, int dst, double step, double omega, bool extrap) {
+    const R* vcr = Vr[vcur];
+    const R* vci = Vi[vcur];
+    R* xr = Vr[dst];
+    R* xi = Vi[dst];
+    const R st = (R)step, om = (R)omega;
+    double pw = 0.0;
+    cgemm_smem<R, 2, 2, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg,
+                              [&](int p, int q, R gr, R gi) {
+                                const int o = p * ldv + q;
+                                R vr = vcr[o], vi = vci[o];
+                                if (extrap) {
+                                  vr = vr + om * (vr - xr[o]);
+                                  vi = vi + om * (vi - xi[o]);
+                                }
+                                const R x_r = vr - st * gr, x_i = vi - st * gi;
+                                xr[o] = x_r;
+                                xi[o] = x_i;
+                                pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
+                              });
+    pw = block_sum(pw, red);
+    if (tid == 0) xs[XS_POWER] = pw;
+    cl.sync();
+    return xsum(XS_POWER);
+  };
+  auto gemm_hv = [&](int src, int dst) {
+    R* gr = Gr[dst];
+    R* gi = Gi[dst];
+    cgemm_smem<R, 2, 2, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv,
+                               [&](int p, int q, R cr, R ci) {
+                                 gr[p * ldg + q] = cr;
+                                 gi[p * ldg + q] = ci;
+                               });
+  };
+
+  for (;;) {
+    if (crank == 0 && tid == 0) s_r = atomicAdd(a.counter, 1ULL);
+    cl.sync();
+    const long long r = (long long)*cl.map_shared_rank(&s_r, 0);
+    if (r >= a.B) {
+      cl.sync();  // rank 0 stays alive until every CTA has read s_r
+      break;
+    }
+    // ---------------- load realization r: full H, own columns of V0 ----------------
+    {
+      const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
+      for (int i = tid; i < KN * M; i += blockDim.x) {
+        const int row = i / M, col = i - row * M;
+        const RC<R> v = Hg[i];
+        Hr[row * ldh + col] = v.r;
+        Hi[row * ldh + col] = v.i;
+      }
+      const RC<R>* Vg = reinterpret_cast<const RC<R>*>(a.V0) + ((size_t)r * K + k0) * M * DD;
+      for (int i = tid; i < KL * M * DD; i += blockDim.x) {
+        const int kl = i / (M * DD), rem = i - kl * M * DD, m = rem / DD, s = rem - m * DD;
+        const RC<R> v = Vg[i];
+        Vr[0][m * ldv + kl * DD + s] = v.r;
+        Vi[0][m * ldv + kl * DD + s] = v.i;
+      }
+      for (int kl = tid; kl < KL; kl += blockDim.x) {
+        alpha[kl] = a.alpha[(size_t)r * K + k0 + kl];
+        lndetw[kl] = 0.0;
+        for (int p = 0; p < DD; ++p)
+          for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
+      }
+      if (tid == 0) {
+        ctl.sigma2 = a.sigma2[r];
+        ctl.pmax = a.pmax[r];
+        ctl.omega = a.omega_arr ? a.omega_arr[r] : a.omega;
+        ctl.nhist = 0;
+        ctl.wsr_last = ctl.wsr_prev = 0.0;
+        ctl.running_max = -INFINITY;
+        ctl.drop_streak = 0;
+        ctl.latched = 0;
+        ctl.switch_it = -1;
+        ctl.weighted_now = 0;
+        ctl.last_weighted = 0;
+        ctl.cur = 0;
+        ctl.stop = 0;
+        ctl.status = 0;
+        ctl.converged = 0;
+        ctl.iters = 0;
+        ctl.f_u = ctl.f_w = ctl.f_v = ctl.wsr = 0.0;
+      }
+    }
+    __syncthreads();
+    // ---------------- bounds (objective.py:216-240): own users, max over cluster ----------------
+    {
+      // Grams of H rows of ALL users over M would duplicate work; own users only
+      const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+      for (int kl = warp; kl < KL; kl += nw) {
+        const int k = k0 + kl;
+        double sr[NN][NN], si[NN][NN];
+        for (int p = 0; p < NN; ++p)
+          for (int q = 0; q < NN; ++q) sr[p][q] = si[p][q] = 0.0;
+        for (int m = lane; m < M; m += 32) {
+          double hr[NN], hi[NN];
+          for (int p = 0; p < NN; ++p) {
+            hr[p] = (double)Hr[(k * NN + p) * ldh + m];
+            hi[p] = (double)Hi[(k * NN + p) * ldh + m];
+          }
+          for (int p = 0; p < NN; ++p)
+            for (int q = 0; q < NN; ++q) {
+              sr[p][q] = fma(hr[p], hr[q], fma(hi[p], hi[q], sr[p][q]));
+              si[p][q] = fma(hi[p], hr[q], fma(-hr[p], hi[q], si[p][q]));
+            }
+        }
+        cd G[NN][NN];
+        for (int p = 0; p < NN; ++p)
+          for (int q = 0; q < NN; ++q) G[p][q] = cmk(warp_allsum(sr[p][q]), warp_allsum(si[p][q]));
+        if (lane == 0) rate[kl] = herm_eig_max<NN>(G);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double kap = 0.0;
+        for (int kl = 0; kl < KL; ++kl) kap = fmax(kap, rate[kl]);
+        xs[XS_KAPPA] = kap;
+      }
+      cl.sync();
+      if (tid == 0) {
+        double kappa = 0.0;
+        for (int c = 0; c < C; ++c) kappa = fmax(kappa, cl.map_shared_rank(xs, c)[XS_KAPPA]);
+        double abar = a.alpha[(size_t)r * K];
+        for (int k = 0; k < K; ++k) abar = fmax(abar, a.alpha[(size_t)r * K + k]);
+        const double l_v = 2.0 * abar * K * kappa / ctl.sigma2;
+        ctl.gamma_safe = 1.0 / l_v;
+        ctl.gamma = a.gamma_arr ? a.gamma_arr[r] : (a.gamma_safe ? ctl.gamma_safe : a.gamma);
+        ctl.step = 2.0 * ctl.gamma;
+        if (crank == 0 && a.gamma_used) a.gamma_used[r] = ctl.gamma;
+      }
+    }
+    gemm_hv(0, 0);
+    __syncthreads();
+
+    // ---------------- main loop (solvers.py:440-505) ----------------
+    for (int t = 1; t <= a.max_iters; ++t) {
+      const int cur = ctl.cur, oth = 1 - cur;
+      if (tid == 0) {  // stage test (solvers.py:449-459), identical in every CTA
+        int wn;
+        if (ctl.latched) {
+          wn = 1;
+        } else {
+          double rs = INFINITY;
+          if (ctl.nhist >= 2) {
+            const double den = fabs(ctl.wsr_prev);
+            rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
+          }
+          wn = rs <= a.eps1;
+          if (wn) {
+            if (a.latch) ctl.latched = 1;
+            if (ctl.switch_it < 0) ctl.switch_it = t;
+          }
+        }
+        ctl.weighted_now = wn;
+      }
+      const bool extrap = (t >= 2) && (ctl.omega > 0.0);
+      {
+        const R om = (R)ctl.omega;
+        R *gcr = Gr[cur], *gci = Gi[cur], *gwr = Gr[oth], *gwi = Gi[oth];
+        for (int i = tid; i < KN * ncol; i += blockDim.x) {
+          R xr = gcr[i], xi = gci[i];
+          if (extrap) {
+            xr = xr + om * (xr - gwr[i]);
+            xi = xi + om * (xi - gwi[i]);
+          }
+          gwr[i] = xr;
+          gwi[i] = xi;
+        }
+      }
+      __syncthreads();
+      gram_partials(Gr[oth], Gi[oth], 0);
+      cl.sync();
+      k1_phase(oth, ctl.weighted_now, true);
+      if (tid == 0) {
+        ctl.f_u = xsum(XS_FU);
+        ctl.f_w = xsum(XS_FW);
+        const int st = xfirst(XS_ST1);
+        if (st) {
+          ctl.status = st;
+          ctl.stop = 1;
+        }
+      }
+      __syncthreads();
+      if (ctl.stop) break;
+      build_yhat(oth);
+      __syncthreads();
+      const double power = grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
+      double scale = 1.0;
+      if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
+      if (scale != 1.0) {
+        const R sc = (R)scale;
+        for (int i = tid; i < M * ncol; i += blockDim.x) {
+          Vr[oth][i] *= sc;
+          Vi[oth][i] *= sc;
+        }
+      }
+      __syncthreads();
+      gemm_hv(oth, oth);
+      __syncthreads();
+      gram_partials(Gr[oth], Gi[oth], 1);
+      cl.sync();
+      for (int kl = tid; kl < KL; kl += blockDim.x) {
+        cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
+        gram_of(1, kl, Tg);
+#pragma unroll
+        for (int p = 0; p < NN; ++p)
+#pragma unroll
+          for (int s = 0; s < DD; ++s) {
+            const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
+            Gkk[p][s] = cmk((double)Gr[oth][idx], (double)Gi[oth][idx]);
+            U[p][s] = ucache[(kl * NN + p) * DD + s];
+          }
+#pragma unroll
+        for (int p = 0; p < DD; ++p)
+#pragma unroll
+          for (int q = 0; q < DD; ++q) W[p][q] = wcache[(kl * DD + p) * DD + q];
+        double rr, ff;
+        int st;
+        wsr_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], U, W, lndetw[kl], rr, ff, st);
+        rate[kl] = rr;
+        fv[kl] = ff;
+        ust[kl] = st;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double sr = 0.0, sv = 0.0;
+        int st = 0;
+        for (int kl = 0; kl < KL; ++kl) {
+          sr += rate[kl];
+          sv += fv[kl];
+          if (st == 0 && ust[kl] != 0.0) st = (int)ust[kl];
+        }
+        xs[XS_RATE] = sr;
+        xs[XS_FV] = sv;
+        xs[XS_ST2] = st;
+      }
+      cl.sync();
+      if (tid == 0) {
+        const double wsr = xsum(XS_RATE);
+        const double sv = xsum(XS_FV);
+        int st = xfirst(XS_ST2);
+        const double total_power = scale == 1.0 ? power : power * scale * scale;
+        if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
+        double rel = INFINITY;
+        if (t > 1) {
+          const double den = fabs(ctl.wsr_last);
+          rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
+        }
+        ctl.wsr_prev = ctl.wsr_last;
+        ctl.wsr_last = wsr;
+        ctl.nhist += 1;
+        ctl.iters = t;
+        ctl.wsr = wsr;
+        ctl.f_v = sv;
+        ctl.last_weighted = ctl.weighted_now;
+        if (a.trace && crank == 0) {
+          double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
+          tr[AMMMSE_TRACE_T] = (double)t;
+          tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
+          tr[AMMMSE_TRACE_F_VALUE] = sv;
+          tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
+          tr[AMMMSE_TRACE_STAGE] = (double)ctl.weighted_now;
+          tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
+          tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
+          tr[AMMMSE_TRACE_F_AFTER_V] = sv;
+          tr[AMMMSE_TRACE_REL_CHANGE] = rel;
+        }
+        ctl.running_max = fmax(ctl.running_max, wsr);
+        if (wsr < 0.5 * ctl.running_max)
+          ctl.drop_streak += 1;
+        else
+          ctl.drop_streak = 0;
+        if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
+        if (st) {
+          ctl.status = st;
+          ctl.stop = 1;
+        } else {
+          ctl.cur = oth;
+          if (ctl.weighted_now && rel <= a.eps2) {
+            ctl.converged = 1;
+            ctl.stop = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (ctl.stop) break;
+    }
+
+    // ---------------- exit: stationarity residual (solvers.py:400-412) ----------------
+    double residual = NAN;
+    if (ctl.status == 0) {
+      const int cur = ctl.cur, oth = 1 - cur;
+      const bool weighted = ctl.latched || ctl.last_weighted;
+      for (int i = tid; i < KN * ncol; i += blockDim.x) {
+        Gr[oth][i] = Gr[cur][i];
+        Gi[oth][i] = Gi[cur][i];
+      }
+      __syncthreads();
+      gram_partials(Gr[oth], Gi[oth], 0);
+      cl.sync();
+      k1_phase(oth, weighted, false);
+      int st = xfirst(XS_ST1);
+      __syncthreads();
+      if (st == 0) {
+        build_yhat(oth);
+        __syncthreads();
+        const double power = grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false);
+        double scale = 1.0;
+        if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
+        double dsum = 0.0, vsum = 0.0;
+        for (int i = tid; i < M * ncol; i += blockDim.x) {
+          const double a_r = (double)Vr[cur][i], a_i = (double)Vi[cur][i];
+          const double dr = a_r - (double)((R)(Vr[oth][i] * (R)scale));
+          const double di = a_i - (double)((R)(Vi[oth][i] * (R)scale));
+          dsum += dr * dr + di * di;
+          vsum += a_r * a_r + a_i * a_i;
+        }
+        dsum = block_sum(dsum, red);
+        vsum = block_sum(vsum, red);
+        if (tid == 0) {
+          xs[XS_DSUM] = dsum;
+          xs[XS_VSUM] = vsum;
+        }
+        cl.sync();
+        residual = sqrt(xsum(XS_DSUM)) / fmax(1.0, sqrt(fmax(xsum(XS_VSUM), 0.0)));
+      } else if (tid == 0) {
+        ctl.status = st;
+      }
+    }
+    __syncthreads();
+    // ---------------- write results (own users' precoders) ----------------
+    {
+      const int cur = ctl.cur;
+      if (a.Vout) {
+        RC<R>* Vg = reinterpret_cast<RC<R>*>(a.Vout) + ((size_t)r * K + k0) * M * DD;
+        for (int i = tid; i < KL * M * DD; i += blockDim.x) {
+          const int kl = i / (M * DD), rem = i - kl * M * DD, m = rem / DD, s = rem - m * DD;
+          Vg[i] = RC<R>{Vr[cur][m * ldv + kl * DD + s], Vi[cur][m * ldv + kl * DD + s]};
+        }
+      }
+      if (tid == 0 && crank == 0) {
+        if (a.wsr_bits) a.wsr_bits[r] = ctl.wsr / kLn2;
+        if (a.iterations) a.iterations[r] = ctl.iters;
+        if (a.converged) a.converged[r] = (unsigned char)ctl.converged;
+        if (a.residual) a.residual[r] = residual;
+        if (a.switch_it) a.switch_it[r] = ctl.switch_it;
+        if (a.status) a.status[r] = ctl.status;
+      }
+    }
+    // all remote reads of this realization's exchange buffers are complete
+    // before any CTA starts the next realization (its first writes)
+    cl.sync();
+  }
+}
+
+}  // namespace ammmse

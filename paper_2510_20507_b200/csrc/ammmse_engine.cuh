@@ -36,6 +36,7 @@
 
 #include "ammmse.h"
 #include "small_linalg.cuh"
+#include "user_algebra.cuh"
 
 namespace ammmse {
 
@@ -311,235 +312,73 @@ struct Engine {
   }
 
   // Receiver / weight / gradient-factor update of user k from the Gram in
-  // `gram` and the work G in buffer w (Ĝ).  Writes U/P/D (R) for the Ŷ
-  // phase and the fp64 caches.  Returns a per-user status in ustat[k].
+  // `gram` and the work G (Ĝ).  Writes U/P/D (R) for the Ŷ phase, the fp64
+  // U/W caches and the per-user objective terms / status.
   __device__ void k1_user(int k, const R* Gwr, const R* Gwi, int ldg, double sigma2, bool weighted,
                           bool want_f) {
-    cd A[NN][NN];
+    cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
-      for (int b = 0; b < NN; ++b) A[a][b] = gram[(k * NN + a) * NN + b];
-#pragma unroll
-    for (int a = 0; a < NN; ++a) A[a][a].r += sigma2;
-    cd Lc[NN][NN];
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b < NN; ++b) Lc[a][b] = A[a][b];
-    double st = 0.0;
-    if (!chol_lower<NN>(Lc)) st = AMMMSE_STATUS_NONFINITE;
-    // G_kk (N x d) and U = A^{-1} G_kk
-    cd Gkk[NN][DD], U[NN][DD];
+      for (int b = 0; b < NN; ++b) Tg[a][b] = gram[(k * NN + a) * NN + b];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
       for (int s = 0; s < DD; ++s) {
         const int idx = (k * NN + a) * ldg + k * DD + s;
         Gkk[a][s] = cmk((double)Gwr[idx], (double)Gwi[idx]);
-        U[a][s] = Gkk[a][s];
-      }
-    chol_solve<NN, DD>(Lc, U);
-    // T = I - U^H G_kk   (the weight-update argument, solvers.py:242)
-    cd T[DD][DD];
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) {
-        cd s = cmk(0.0);
-#pragma unroll
-        for (int a = 0; a < NN; ++a) cfmac(s, U[a][p], Gkk[a][q]);
-        T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
-      }
-    double ak = alpha[k];
-    // MSE matrix E (objective.py:84-105) in Gram form:
-    //   E = I - U^H G_kk - G_kk^H U + U^H A U
-    cd E[DD][DD];
-    if (want_f) {
-      cd AU[NN][DD];
-#pragma unroll
-      for (int a = 0; a < NN; ++a)
-#pragma unroll
-        for (int s = 0; s < DD; ++s) {
-          cd acc = cmk(0.0);
-#pragma unroll
-          for (int b = 0; b < NN; ++b) cfma(acc, A[a][b], U[b][s]);
-          AU[a][s] = acc;
-        }
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) {
-          cd uau = cmk(0.0);
-#pragma unroll
-          for (int a = 0; a < NN; ++a) cfmac(uau, U[a][p], AU[a][q]);
-          // (I - U^H G)[p][q] = T[p][q];  (G^H U)[p][q] = conj((U^H G)[q][p]) = conj(δ - T[q][p])
-          const cd ghu = cconj(csub(cmk(p == q ? 1.0 : 0.0), T[q][p]));
-          E[p][q] = cadd(csub(T[p][q], ghu), uau);
-        }
-      // f_after_u with the previous W (solvers.py:447)
-      double tr = 0.0;
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) {
-          const cd w = wcache[(k * DD + p) * DD + q];
-          tr += w.r * E[q][p].r - w.i * E[q][p].i;
-        }
-      fu[k] = ak * (tr - lndetw[k]);
-    }
-    // W update or identity (solvers.py:461-464)
-    cd W[DD][DD];
-    double lw = 0.0;
-    if (weighted) {
-      cd Tc[DD][DD], Ti[DD][DD];
-      double nT = 0.0;
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) { Tc[p][q] = T[p][q]; nT += cabs2(T[p][q]); }
-      bool ok = inverse_gj<DD>(Tc, Ti);
-      double nTi = 0.0;
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) nTi += cabs2(Ti[p][q]);
-      // Frobenius condition estimate; >= the 2-norm cond of np.linalg.cond
-      const double cond = sqrt(nT) * sqrt(nTi);
-      if (!ok || !isfinite(cond) || cond > kCondLimit) {
-        if (st == 0.0) st = AMMMSE_STATUS_ILL_CONDITIONED;
-      }
-      // hermitianize (linalg.py:12-14)
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q)
-          W[p][q] = cmk(0.5 * (Ti[p][q].r + Ti[q][p].r), 0.5 * (Ti[p][q].i - Ti[q][p].i));
-      cd LW[DD][DD];
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) LW[p][q] = W[p][q];
-      if (!chol_lower<DD>(LW)) {  // eigvalsh(W)[0] <= 0  (solvers.py:249-252)
-        if (st == 0.0) st = AMMMSE_STATUS_ILL_CONDITIONED;
-        lw = 0.0;
-      } else {
-        lw = chol_lndet<DD>(LW);
-      }
-    } else {
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) W[p][q] = cmk(p == q ? 1.0 : 0.0);
-    }
-    if (want_f) {
-      double tr = 0.0;
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) tr += W[p][q].r * E[q][p].r - W[p][q].i * E[q][p].i;
-      fw[k] = ak * (tr - lw);
-    }
-    // P = α U W (N x d);  D = -P T = α U W (U^H G_kk - I)  (diagonal block of Ŷ)
-    cd Pm[NN][DD];
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) {
-        cd acc = cmk(0.0);
-#pragma unroll
-        for (int p = 0; p < DD; ++p) cfma(acc, U[a][p], W[p][q]);
-        Pm[a][q] = cscale(acc, ak);
-      }
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) {
-        cd acc = cmk(0.0);
-#pragma unroll
-        for (int p = 0; p < DD; ++p) cfma(acc, Pm[a][p], T[p][q]);
-        const int o = (k * NN + a) * DD + q;
-        Df[o] = RC<R>{(R)(-acc.r), (R)(-acc.i)};
-        Pf[o] = RC<R>{(R)Pm[a][q].r, (R)Pm[a][q].i};
-        Uf[o] = RC<R>{(R)U[a][q].r, (R)U[a][q].i};
-        ucache[o] = U[a][q];
       }
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
-      for (int q = 0; q < DD; ++q) wcache[(k * DD + p) * DD + q] = W[p][q];
-    lndetw[k] = lw;
-    ustat[k] = st;
+      for (int q = 0; q < DD; ++q) Wp[p][q] = wcache[(k * DD + p) * DD + q];
+    K1Out<NN, DD> o;
+    k1_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], Wp, lndetw[k], weighted, want_f, o);
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        const int i = (k * NN + a) * DD + q;
+        Df[i] = RC<R>{(R)o.D[a][q].r, (R)o.D[a][q].i};
+        Pf[i] = RC<R>{(R)o.P[a][q].r, (R)o.P[a][q].i};
+        Uf[i] = RC<R>{(R)o.U[a][q].r, (R)o.U[a][q].i};
+        ucache[i] = o.U[a][q];
+      }
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) wcache[(k * DD + p) * DD + q] = o.W[p][q];
+    lndetw[k] = o.lndetw;
+    fu[k] = o.fu;
+    fw[k] = o.fw;
+    ustat[k] = o.status;
   }
 
   // Rate and f_after_v terms of user k from the Gram of G_new.
   __device__ void wsr_user(int k, const R* Gnr, const R* Gni, int ldg, double sigma2) {
-    cd A[NN][NN], Cv[NN][NN], Gkk[NN][DD];
+    cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) Tg[a][b] = gram[(k * NN + a) * NN + b];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
       for (int s = 0; s < DD; ++s) {
         const int idx = (k * NN + a) * ldg + k * DD + s;
         Gkk[a][s] = cmk((double)Gnr[idx], (double)Gni[idx]);
+        U[a][s] = ucache[(k * NN + a) * DD + s];
       }
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b < NN; ++b) {
-        A[a][b] = gram[(k * NN + a) * NN + b];
-        cd own = cmk(0.0);
-#pragma unroll
-        for (int s = 0; s < DD; ++s) own = cadd(own, cmulcb(Gkk[a][s], Gkk[b][s]));
-        Cv[a][b] = csub(A[a][b], own);
-      }
-#pragma unroll
-    for (int a = 0; a < NN; ++a) {
-      A[a][a].r += sigma2;
-      A[a][a].i = 0.0;
-      Cv[a][a].r += sigma2;
-      Cv[a][a].i = 0.0;
-    }
-    // f_after_v with this iteration's U, W at the new precoders (solvers.py:471)
-    cd U[NN][DD];
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int s = 0; s < DD; ++s) U[a][s] = ucache[(k * NN + a) * DD + s];
-    double tr = 0.0;
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
-      for (int q = 0; q < DD; ++q) {
-        cd uhg = cmk(0.0), ghu = cmk(0.0), uau = cmk(0.0);
-#pragma unroll
-        for (int a = 0; a < NN; ++a) {
-          cfmac(uhg, U[a][p], Gkk[a][q]);
-          cfmac(ghu, Gkk[a][p], U[a][q]);
-          cd au = cmk(0.0);
-#pragma unroll
-          for (int b = 0; b < NN; ++b) cfma(au, A[a][b], U[b][q]);
-          cfmac(uau, U[a][p], au);
-        }
-        cd e = csub(csub(uau, uhg), ghu);
-        if (p == q) e.r += 1.0;
-        // accumulate Tr(W E): W[q][p] * E[p][q]
-        const cd w = wcache[(k * DD + q) * DD + p];
-        tr += w.r * e.r - w.i * e.i;
-      }
-    fv[k] = alpha[k] * (tr - lndetw[k]);
-    // rate (objective.py:108-128), clipped at 0
-    double r = 0.0;
-    bool ok1 = chol_lower<NN>(A);
-    bool ok2 = chol_lower<NN>(Cv);
-    if (ok1 && ok2) {
-      r = chol_lndet<NN>(A) - chol_lndet<NN>(Cv);
-      r = r > 0.0 ? r : 0.0;
-      rate[k] = alpha[k] * r;
-      ustat[k] = 0.0;
-    } else {
-      rate[k] = 0.0;
-      ustat[k] = AMMMSE_STATUS_NONFINITE;
-    }
+      for (int q = 0; q < DD; ++q) W[p][q] = wcache[(k * DD + p) * DD + q];
+    double r, f;
+    int st;
+    wsr_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], U, W, lndetw[k], r, f, st);
+    rate[k] = r;
+    fv[k] = f;
+    ustat[k] = st;
   }
 
   // Ŷ in place over the work G: (m, j) pairs, j fastest.

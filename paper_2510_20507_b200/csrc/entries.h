@@ -5,9 +5,11 @@
 namespace ammmse {
 
 struct KernelEntry {
-  const void* solve;                    // ammmse_solve_kernel<R, N, d>
-  const void* bounds;                   // ammmse_bounds_kernel<R, N>
-  size_t (*smem_bytes)(int M, int K);   // Layout<R, N, d>::bytes
+  const void* solve;                           // ammmse_solve_kernel<R, N, d>   (1 CTA / realization)
+  const void* bounds;                          // ammmse_bounds_kernel<R, N>
+  size_t (*smem_bytes)(int M, int K);          // Layout<R, N, d>::bytes
+  const void* cluster_solve;                   // ammmse_cluster_kernel<R, N, d> (1 cluster / realization)
+  size_t (*cluster_smem_bytes)(int M, int K, int C);  // CLayout<R, N, d>::bytes
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4

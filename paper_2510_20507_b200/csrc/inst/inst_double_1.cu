@@ -1,9 +1,15 @@
 // Generated instantiation unit: engine kernels for R=double, N=1, d=1..4.
-#include "../ammmse_engine.cuh"
+#include "../ammmse_cluster.cuh"
 #include "../entries.h"
 
 namespace ammmse {
 namespace {
+template <int DD>
+size_t cluster_smem_fn(int M, int K, int C) {
+  CLayout<double, 1, DD> L;
+  L.init(M, K, C);
+  return L.bytes;
+}
 template <int DD>
 size_t smem_fn(int M, int K) {
   Layout<double, 1, DD> L;
@@ -11,10 +17,14 @@ size_t smem_fn(int M, int K) {
   return L.bytes;
 }
 const KernelEntry kEntries[4] = {
-    {(const void*)ammmse_solve_kernel<double, 1, 1>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<1>},
-    {(const void*)ammmse_solve_kernel<double, 1, 2>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<2>},
-    {(const void*)ammmse_solve_kernel<double, 1, 3>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<3>},
-    {(const void*)ammmse_solve_kernel<double, 1, 4>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<4>},
+    {(const void*)ammmse_solve_kernel<double, 1, 1>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<1>,
+     (const void*)ammmse_cluster_kernel<double, 1, 1>, cluster_smem_fn<1>},
+    {(const void*)ammmse_solve_kernel<double, 1, 2>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<2>,
+     (const void*)ammmse_cluster_kernel<double, 1, 2>, cluster_smem_fn<2>},
+    {(const void*)ammmse_solve_kernel<double, 1, 3>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<3>,
+     (const void*)ammmse_cluster_kernel<double, 1, 3>, cluster_smem_fn<3>},
+    {(const void*)ammmse_solve_kernel<double, 1, 4>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<4>,
+     (const void*)ammmse_cluster_kernel<double, 1, 4>, cluster_smem_fn<4>},
 };
 }  // namespace
 const KernelEntry* entries_double_1() { return kEntries; }

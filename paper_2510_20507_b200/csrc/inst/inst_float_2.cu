@@ -1,9 +1,15 @@
 // Generated instantiation unit: engine kernels for R=float, N=2, d=1..4.
-#include "../ammmse_engine.cuh"
+#include "../ammmse_cluster.cuh"
 #include "../entries.h"
 
 namespace ammmse {
 namespace {
+template <int DD>
+size_t cluster_smem_fn(int M, int K, int C) {
+  CLayout<float, 2, DD> L;
+  L.init(M, K, C);
+  return L.bytes;
+}
 template <int DD>
 size_t smem_fn(int M, int K) {
   Layout<float, 2, DD> L;
@@ -11,10 +17,14 @@ size_t smem_fn(int M, int K) {
   return L.bytes;
 }
 const KernelEntry kEntries[4] = {
-    {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>},
-    {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>},
-    {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>},
-    {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>},
+    {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>,
+     (const void*)ammmse_cluster_kernel<float, 2, 1>, cluster_smem_fn<1>},
+    {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>,
+     (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>},
+    {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>,
+     (const void*)ammmse_cluster_kernel<float, 2, 3>, cluster_smem_fn<3>},
+    {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>,
+     (const void*)ammmse_cluster_kernel<float, 2, 4>, cluster_smem_fn<4>},
 };
 }  // namespace
 const KernelEntry* entries_float_2() { return kEntries; }

@@ -1,9 +1,15 @@
 // Generated instantiation unit: engine kernels for R=float, N=3, d=1..4.
-#include "../ammmse_engine.cuh"
+#include "../ammmse_cluster.cuh"
 #include "../entries.h"
 
 namespace ammmse {
 namespace {
+template <int DD>
+size_t cluster_smem_fn(int M, int K, int C) {
+  CLayout<float, 3, DD> L;
+  L.init(M, K, C);
+  return L.bytes;
+}
 template <int DD>
 size_t smem_fn(int M, int K) {
   Layout<float, 3, DD> L;
@@ -11,10 +17,14 @@ size_t smem_fn(int M, int K) {
   return L.bytes;
 }
 const KernelEntry kEntries[4] = {
-    {(const void*)ammmse_solve_kernel<float, 3, 1>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<1>},
-    {(const void*)ammmse_solve_kernel<float, 3, 2>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<2>},
-    {(const void*)ammmse_solve_kernel<float, 3, 3>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<3>},
-    {(const void*)ammmse_solve_kernel<float, 3, 4>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<4>},
+    {(const void*)ammmse_solve_kernel<float, 3, 1>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<1>,
+     (const void*)ammmse_cluster_kernel<float, 3, 1>, cluster_smem_fn<1>},
+    {(const void*)ammmse_solve_kernel<float, 3, 2>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<2>,
+     (const void*)ammmse_cluster_kernel<float, 3, 2>, cluster_smem_fn<2>},
+    {(const void*)ammmse_solve_kernel<float, 3, 3>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<3>,
+     (const void*)ammmse_cluster_kernel<float, 3, 3>, cluster_smem_fn<3>},
+    {(const void*)ammmse_solve_kernel<float, 3, 4>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<4>,
+     (const void*)ammmse_cluster_kernel<float, 3, 4>, cluster_smem_fn<4>},
 };
 }  // namespace
 const KernelEntry* entries_float_3() { return kEntries; }

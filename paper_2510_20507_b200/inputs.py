@@ -143,7 +143,7 @@ WORKLOADS = {
                       1e-5, 500, gamma=0.002, omega=0.8, snr_db=20.0),
     # [3] massive MIMO, Kronecker-correlated
     "massive": Workload("massive", 256, 2, 64, 2, 16384, 100.0, "ones", "kronecker",
-                        np.complex64, 1e-5, 500, gamma=0.001, omega=0.8, snr_db=20.0),
+                        np.complex64, 1e-5, 500, gamma=0.002, omega=0.8, snr_db=20.0),
 }
 # [4] throughput sweep: exactly 50 iterations (eps2 = smallest positive double)
 for _M, _g in ((32, 0.008), (64, 0.004), (128, 0.002), (256, 0.001), (512, 0.0005)):

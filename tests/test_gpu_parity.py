@@ -149,3 +149,37 @@ def test_max_iters_one(cuda):
     assert np.isinf(g.trace[:, 0, 8]).all()
     np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-10)
     np.testing.assert_allclose(g.stationarity_residual, r["stationarity_residual"], rtol=1e-7)
+
+
+@pytest.mark.parametrize("csize", [1, 2, 4])
+def test_cluster_engine_complex128(cuda, csize):
+    """The thread-block-cluster engine (forced) reproduces the fp64 oracle."""
+    b = build_batch(16, 2, 4, 2, 5, p_max=100.0, weights="uniform", dtype=np.complex128, seed0=3)
+    kw = dict(gamma=0.01, omega=0.8, eps2=1e-6, max_iters=120)
+    opts = SolverOptions(algorithm="ammmse", **kw)
+    g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                         record_trace=True, cluster_size=csize)
+    r = oracle_solve(b, **kw)
+    assert np.array_equal(g.iterations, r["iterations"])
+    assert np.array_equal(g.switch_iteration, r["switch_iteration"])
+    np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-9)
+    np.testing.assert_allclose(g.stationarity_residual, r["stationarity_residual"], rtol=1e-6)
+    np.testing.assert_allclose(g.final_precoders, r["final_precoders"], rtol=0, atol=1e-8)
+    for i in range(b.B):
+        n = g.iterations[i]
+        np.testing.assert_allclose(g.trace[i, :n, :8], r["trace"][i, :n, :8], rtol=1e-8, atol=1e-9)
+
+
+@pytest.mark.parametrize("csize", [2, 4, 8])
+def test_cluster_engine_complex64_medium(cuda, csize):
+    w = WORKLOADS["medium_snr10"]
+    b = w.batch(B=4)
+    kw = dict(gamma=w.gamma, omega=w.omega, eps1=w.eps1, eps2=w.eps2, max_iters=w.max_iters)
+    opts = SolverOptions(algorithm="ammmse", **kw)
+    g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                         cluster_size=csize)
+    r = oracle_solve(b, **kw)
+    rel = np.abs(g.wsr_bits - r["wsr_bits"]) / np.abs(r["wsr_bits"])
+    assert rel.max() <= WSR_RTOL_C64
+    ok = nonmarginal_mask(r, w.eps1, w.eps2)
+    assert np.array_equal(g.iterations[ok], r["iterations"][ok])
