@@ -113,6 +113,9 @@ typedef struct AmmmseOptions {
   int32_t cluster_size;/* 0: automatic engine choice.  c >= 1: force the thread-block-cluster
                           engine with c CTAs per realization (c in {1,2,4,8,16}, c | K) —
                           a tuning / testing knob, results are identical up to rounding */
+  int32_t h_placement; /* cluster engine only: 0 auto, 1 H resident in every CTA's SMEM,
+                          2 H streamed from HBM/L2 through a cp.async ring */
+  int32_t reserved;
 } AmmmseOptions;
 
 /* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */

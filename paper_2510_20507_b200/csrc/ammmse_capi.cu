@@ -60,19 +60,20 @@ int max_smem_optin() {
 struct Plan {
   const ammmse::KernelEntry* e;
   int cluster;  // 0: single-CTA engine; >= 1: cluster engine with that many CTAs
+  int hres;     // cluster engine: H resident (1) or streamed (0)
   size_t smem;
   int threads;
 };
 
 int pick_threads(const AmmmseDims* d);
 
-int make_plan(const AmmmseDims* d, int force_c, Plan* p) {
+int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
   const ammmse::KernelEntry* e = lookup(d);
   if (!e) return AMMMSE_ERR_UNSUPPORTED;
   int lim = max_smem_optin();
   if (lim <= 0) lim = 232448;  // sm_100 opt-in limit (no device to query)
   p->e = e;
-  if (force_c == 0) {
+  if (force_c == 0 && h_placement == 0) {
     const size_t s1 = e->smem_bytes(d->M, d->K);
     if (s1 <= (size_t)lim) {
       p->cluster = 0;
@@ -81,18 +82,25 @@ int make_plan(const AmmmseDims* d, int force_c, Plan* p) {
       return AMMMSE_OK;
     }
   }
+  // H resident in every CTA of the smallest cluster that fits, else H streamed
   const int cands[5] = {1, 2, 4, 8, 16};
-  for (int i = 0; i < 5; ++i) {
-    const int c = cands[i];
-    if (force_c && c != force_c) continue;
-    if (!force_c && c == 1) continue;
-    if (d->K % c) continue;
-    const size_t s = e->cluster_smem_bytes(d->M, d->K, c);
-    if (s <= (size_t)lim) {
-      p->cluster = c;
-      p->smem = s;
-      p->threads = 256;
-      return AMMMSE_OK;
+  for (int hres = 1; hres >= 0; --hres) {
+    if ((h_placement == 1 && !hres) || (h_placement == 2 && hres)) continue;
+    for (int i = 0; i < 5; ++i) {
+      const int c = cands[i];
+      if (force_c && c != force_c) continue;
+      if (!force_c && c == 1) continue;
+      if (d->K % c) continue;
+      // streamed H moves 16-byte pieces: complex64 rows need an even length
+      if (!hres && d->dtype == AMMMSE_COMPLEX64 && (d->M % 2)) continue;
+      const size_t s = e->cluster_smem_bytes(d->M, d->K, c, hres);
+      if (s <= (size_t)lim) {
+        p->cluster = c;
+        p->hres = hres;
+        p->smem = s;
+        p->threads = 256;
+        return AMMMSE_OK;
+      }
     }
   }
   return AMMMSE_ERR_UNSUPPORTED;
@@ -125,7 +133,7 @@ int ammmse_check_dims(const AmmmseDims* dims) {
   int rc = dims_valid(dims);
   if (rc) return rc;
   Plan p;
-  return make_plan(dims, 0, &p);
+  return make_plan(dims, 0, 0, &p);
 }
 
 size_t ammmse_workspace_size(const AmmmseDims* dims) {
@@ -171,7 +179,8 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     return AMMMSE_ERR_WORKSPACE;
   }
   Plan plan;
-  if (opt->cluster_size < 0 || make_plan(dims, opt->cluster_size, &plan) != AMMMSE_OK) {
+  if (opt->cluster_size < 0 || opt->h_placement < 0 || opt->h_placement > 2 ||
+      make_plan(dims, opt->cluster_size, opt->h_placement, &plan) != AMMMSE_OK) {
     snprintf(g_err, sizeof g_err, "no engine configuration fits (cluster_size %d)", opt->cluster_size);
     return AMMMSE_ERR_UNSUPPORTED;
   }
@@ -257,6 +266,7 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.M = dims->M;
   a.K = dims->K;
   a.B = dims->batch;
+  a.hres = plan.cluster ? plan.hres : 1;
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
   void* args[] = {&a};
   if (plan.cluster)

@@ -33,14 +33,142 @@ enum XSlot {
   XS_ST3, XS_COUNT
 };
 
+// ---------------------------------------------------------------------------
+// Streamed complex GEMM for realizations whose H does not fit in SMEM.
+//   C(p,q) = sum_k A(p,k) B(k,q),  B planar in SMEM (B[k*ldb+q])
+//   CONJT : A(p,k) = conj(H[k][p])   chunk = H rows [k0, k0+KC)      (KC x P, contiguous)
+//   !CONJT: A(p,k) = H[p][k]         chunk = H cols [k0, k0+KC)      (P x KC, row segments)
+// H (global, interleaved complex, row length ldH) is staged chunk by chunk
+// through a double-buffered SMEM ring with cp.async (16-byte pieces), the
+// next chunk in flight while the current one is consumed.  Every thread
+// owns up to TPT register tiles of RY x RX outputs for the whole K loop.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename R, int RY, int RX, int TPT, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* __restrict__ Hg,
+                                             int ldH, RC<R>* __restrict__ stage, int SB,
+                                             const R* __restrict__ Br, const R* __restrict__ Bi,
+                                             int ldb, Epi epi) {
+  constexpr int EPC = 16 / sizeof(RC<R>);  // complex elements per 16-byte piece (2 or 1)
+  const int KC0 = SB / P;                  // chunk extent along k
+  const int KC = CONJT ? KC0 : (KC0 / EPC) * EPC;
+  const int lds = CONJT ? P : KC + EPC;     // staging row stride (elements), 16 B aligned
+  const int nchunks = (KD + KC - 1) / KC;
+  const int QT = (Q + RX - 1) / RX, PT = (P + RY - 1) / RY, ntiles = PT * QT;
+
+  auto issue = [&](int c, int buf) {
+    const int k0 = c * KC;
+    const int kc = min(KC, KD - k0);
+    RC<R>* dst = stage + (size_t)buf * SB;
+    if (CONJT) {  // rows k0..k0+kc of H, each P long: contiguous block
+      const RC<R>* src = Hg + (size_t)k0 * ldH;
+      const int pieces = (kc * P) / EPC;
+      for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
+        const int e = i * EPC, row = e / P, col = e - row * P;
+        cp_async16(dst + row * lds + col, src + (size_t)row * ldH + col);
+      }
+    } else {      // columns k0..k0+kc of every row p
+      const int ppr = kc / EPC;  // pieces per row (kc multiple of EPC except the tail)
+      for (int i = threadIdx.x; i < P * ppr; i += blockDim.x) {
+        const int row = i / ppr, e = (i - row * ppr) * EPC;
+        cp_async16(dst + row * lds + e, Hg + (size_t)row * ldH + k0 + e);
+      }
+    }
+    cp_async_commit();
+  };
+
+  R cr[TPT][RY][RX], ci[TPT][RY][RX];
+#pragma unroll
+  for (int t = 0; t < TPT; ++t)
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j) cr[t][i][j] = ci[t][i][j] = R(0);
+
+  issue(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      issue(c + 1, (c + 1) & 1);
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    const RC<R>* A = stage + (size_t)(c & 1) * SB;
+    const int k0 = c * KC, kc = min(KC, KD - k0);
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      const int tile = threadIdx.x + t * blockDim.x;
+      if (tile >= ntiles) break;
+      const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
+      int pi[RY], qj[RX];
+#pragma unroll
+      for (int i = 0; i < RY; ++i) pi[i] = min(p0 + i, P - 1);
+#pragma unroll
+      for (int j = 0; j < RX; ++j) qj[j] = min(q0 + j, Q - 1);
+      for (int kk = 0; kk < kc; ++kk) {
+        R ar[RY], ai[RY], br[RX], bi[RX];
+#pragma unroll
+        for (int i = 0; i < RY; ++i) {
+          const RC<R> v = CONJT ? A[kk * lds + pi[i]] : A[pi[i] * lds + kk];
+          ar[i] = v.r;
+          ai[i] = v.i;
+        }
+#pragma unroll
+        for (int j = 0; j < RX; ++j) {
+          br[j] = Br[(k0 + kk) * ldb + qj[j]];
+          bi[j] = Bi[(k0 + kk) * ldb + qj[j]];
+        }
+#pragma unroll
+        for (int i = 0; i < RY; ++i)
+#pragma unroll
+          for (int j = 0; j < RX; ++j) {
+            if (CONJT) {
+              cr[t][i][j] = fma(ar[i], br[j], fma(ai[i], bi[j], cr[t][i][j]));
+              ci[t][i][j] = fma(ar[i], bi[j], fma(-ai[i], br[j], ci[t][i][j]));
+            } else {
+              cr[t][i][j] = fma(ar[i], br[j], fma(-ai[i], bi[j], cr[t][i][j]));
+              ci[t][i][j] = fma(ar[i], bi[j], fma(ai[i], br[j], ci[t][i][j]));
+            }
+          }
+      }
+    }
+    __syncthreads();  // buffer (c & 1) may be refilled by the next issue
+  }
+#pragma unroll
+  for (int t = 0; t < TPT; ++t) {
+    const int tile = threadIdx.x + t * blockDim.x;
+    if (tile >= ntiles) break;
+    const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j)
+        if (p0 + i < P && q0 + j < Q) epi(p0 + i, q0 + j, cr[t][i][j], ci[t][i][j]);
+  }
+}
+
+constexpr int kStreamRY = 4, kStreamRX = 2, kStreamTPT = 4;
+
 template <typename R, int NN, int DD>
 struct CLayout {
   int M, K, C, KL, KN, KD, ncol, ldh, ldv, ldg;
+  int hres;  // 1: H resident in SMEM;  0: H streamed from global through `stage`
+  int SB;    // staging buffer size (complex elements) when streamed
   size_t nH, nV, nG;
   size_t oH, oV0, oV1, oG0, oG1, oUall, oPall, oDown;  // R offsets (planar / RC)
   size_t dbl_off, bytes;
 
-  __host__ __device__ void init(int M_, int K_, int C_) {
+  __host__ __device__ void init(int M_, int K_, int C_, int hres_ = 1) {
+    hres = hres_;
+    SB = 16384 / (int)(2 * sizeof(R));  // 16 KB per staging buffer
     M = M_;
     K = K_;
     C = C_;
@@ -51,9 +179,11 @@ struct CLayout {
     ldh = M | 1;
     ldv = ncol;
     ldg = ncol;
-    nH = (size_t)KN * ldh;
     nV = (size_t)M * ldv;
     nG = (size_t)KN * ldg;
+    // resident: planar H (2 planes of KN x ldh); streamed: 2 buffers of SB interleaved
+    // complex elements = 4 SB reals = 2 "planes" of 2 SB
+    nH = hres ? (size_t)KN * ldh : (size_t)2 * SB;
     oH = 0;
     oV0 = oH + 2 * nH;
     oV1 = oV0 + 2 * nV;
@@ -86,7 +216,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
   const int tid = threadIdx.x;
 
   CLayout<R, NN, DD> L;
-  L.init(a.M, a.K, C);
+  L.init(a.M, a.K, C, a.hres);
+  const bool hres = a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
   const int k0 = crank * KL;       // first own user
@@ -95,6 +226,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
   R* base = reinterpret_cast<R*>(smem);
   R* Hr = base + L.oH;
   R* Hi = Hr + L.nH;
+  RC<R>* stage = reinterpret_cast<RC<R>*>(base + L.oH);  // streamed mode
+  const RC<R>* Hcur = nullptr;                            // this realization's H in global
   R *Vr[2], *Vi[2], *Gr[2], *Gi[2];
   Vr[0] = base + L.oV0; Vi[0] = Vr[0] + L.nV;
   Vr[1] = base + L.oV1; Vi[1] = Vr[1] + L.nV;
@@ -274,8 +407,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
     R* xi = Vi[dst];
     const R st = (R)step, om = (R)omega;
     double pw = 0.0;
-    cgemm_smem<R, 2, 2, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg,
-                              [&](int p, int q, R gr, R gi) {
+    auto epi = [&](int p, int q, R gr, R gi) {
                                 const int o = p * ldv + q;
                                 R vr = vcr[o], vi = vci[o];
                                 if (extrap) {
@@ -286,7 +418,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
                                 xr[o] = x_r;
                                 xi[o] = x_i;
                                 pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
-                              });
+                              };
+    if (hres)
+      cgemm_smem<R, 2, 2, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
+    else
+      cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, true>(M, ncol, KN, Hcur, M, stage, L.SB,
+                                                              Gr[ysrc], Gi[ysrc], ldg, epi);
     pw = block_sum(pw, red);
     if (tid == 0) xs[XS_POWER] = pw;
     cl.sync();
@@ -295,11 +432,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
   auto gemm_hv = [&](int src, int dst) {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
-    cgemm_smem<R, 2, 2, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv,
-                               [&](int p, int q, R cr, R ci) {
-                                 gr[p * ldg + q] = cr;
-                                 gi[p * ldg + q] = ci;
-                               });
+    auto epi = [&](int p, int q, R cr, R ci) {
+      gr[p * ldg + q] = cr;
+      gi[p * ldg + q] = ci;
+    };
+    if (hres)
+      cgemm_smem<R, 2, 2, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
+    else
+      cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, false>(KN, ncol, M, Hcur, M, stage, L.SB,
+                                                               Vr[src], Vi[src], ldv, epi);
   };
 
   for (;;) {
@@ -313,11 +454,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
     // ---------------- load realization r: full H, own columns of V0 ----------------
     {
       const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
-      for (int i = tid; i < KN * M; i += blockDim.x) {
-        const int row = i / M, col = i - row * M;
-        const RC<R> v = Hg[i];
-        Hr[row * ldh + col] = v.r;
-        Hi[row * ldh + col] = v.i;
+      Hcur = Hg;
+      if (hres) {
+        for (int i = tid; i < KN * M; i += blockDim.x) {
+          const int row = i / M, col = i - row * M;
+          const RC<R> v = Hg[i];
+          Hr[row * ldh + col] = v.r;
+          Hi[row * ldh + col] = v.i;
+        }
       }
       const RC<R>* Vg = reinterpret_cast<const RC<R>*>(a.V0) + ((size_t)r * K + k0) * M * DD;
       for (int i = tid; i < KL * M * DD; i += blockDim.x) {
@@ -365,8 +509,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         for (int m = lane; m < M; m += 32) {
           double hr[NN], hi[NN];
           for (int p = 0; p < NN; ++p) {
-            hr[p] = (double)Hr[(k * NN + p) * ldh + m];
-            hi[p] = (double)Hi[(k * NN + p) * ldh + m];
+            if (hres) {
+              hr[p] = (double)Hr[(k * NN + p) * ldh + m];
+              hi[p] = (double)Hi[(k * NN + p) * ldh + m];
+            } else {
+              const RC<R> v = Hcur[(size_t)(k * NN + p) * M + m];
+              hr[p] = (double)v.r;
+              hi[p] = (double)v.i;
+            }
           }
           for (int p = 0; p < NN; ++p)
             for (int q = 0; q < NN; ++q) {

@@ -74,6 +74,7 @@ struct EngineArgs {
   int max_iters;
   int latch;
   int M, K;
+  int hres;  // cluster engine: H resident in SMEM (1) or streamed from global (0)
   long long B;
   unsigned long long* counter;
 };

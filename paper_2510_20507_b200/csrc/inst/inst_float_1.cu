@@ -5,9 +5,9 @@
 namespace ammmse {
 namespace {
 template <int DD>
-size_t cluster_smem_fn(int M, int K, int C) {
+size_t cluster_smem_fn(int M, int K, int C, int hres) {
   CLayout<float, 1, DD> L;
-  L.init(M, K, C);
+  L.init(M, K, C, hres);
   return L.bytes;
 }
 template <int DD>

@@ -170,16 +170,31 @@ def test_cluster_engine_complex128(cuda, csize):
         np.testing.assert_allclose(g.trace[i, :n, :8], r["trace"][i, :n, :8], rtol=1e-8, atol=1e-9)
 
 
-@pytest.mark.parametrize("csize", [2, 4, 8])
-def test_cluster_engine_complex64_medium(cuda, csize):
+@pytest.mark.parametrize("csize,hp", [(2, 1), (4, 1), (8, 1), (4, 2)])
+def test_cluster_engine_complex64_medium(cuda, csize, hp):
     w = WORKLOADS["medium_snr10"]
     b = w.batch(B=4)
     kw = dict(gamma=w.gamma, omega=w.omega, eps1=w.eps1, eps2=w.eps2, max_iters=w.max_iters)
     opts = SolverOptions(algorithm="ammmse", **kw)
     g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
-                         cluster_size=csize)
+                         cluster_size=csize, h_placement=hp)
     r = oracle_solve(b, **kw)
     rel = np.abs(g.wsr_bits - r["wsr_bits"]) / np.abs(r["wsr_bits"])
     assert rel.max() <= WSR_RTOL_C64
     ok = nonmarginal_mask(r, w.eps1, w.eps2)
     assert np.array_equal(g.iterations[ok], r["iterations"][ok])
+
+
+@pytest.mark.parametrize("M,N,K,d,csize", [(16, 2, 4, 2, 2), (12, 4, 4, 4, 4), (10, 1, 4, 2, 2)])
+def test_cluster_engine_streamed_h_complex128(cuda, M, N, K, d, csize):
+    """Streamed-H cluster mode (H through the cp.async ring), forced on small fp64
+    shapes, against the oracle."""
+    b = build_batch(M, N, K, d, 3, p_max=50.0, weights="uniform", dtype=np.complex128, seed0=9)
+    kw = dict(gamma=0.005, omega=0.7, eps2=1e-6, max_iters=80)
+    opts = SolverOptions(algorithm="ammmse", **kw)
+    g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                         record_trace=True, cluster_size=csize, h_placement=2)
+    r = oracle_solve(b, **kw)
+    assert np.array_equal(g.iterations, r["iterations"])
+    np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-9)
+    np.testing.assert_allclose(g.final_precoders, r["final_precoders"], rtol=0, atol=1e-8)
