@@ -57,9 +57,10 @@ __device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* 
                                              const R* __restrict__ Br, const R* __restrict__ Bi,
                                              int ldb, Epi epi) {
   constexpr int EPC = 16 / sizeof(RC<R>);  // complex elements per 16-byte piece (2 or 1)
-  const int KC0 = SB / P;                  // chunk extent along k
-  const int KC = CONJT ? KC0 : (KC0 / EPC) * EPC;
-  const int lds = CONJT ? P : KC + EPC;     // staging row stride (elements), 16 B aligned
+  // chunk extent along k; !CONJT rows are padded by EPC elements (bank spread,
+  // 16-byte aligned row starts), so P * (KC + EPC) <= SB
+  const int KC = CONJT ? SB / P : ((SB / P - EPC) / EPC) * EPC;
+  const int lds = CONJT ? P : KC + EPC;     // staging row stride (elements)
   const int nchunks = (KD + KC - 1) / KC;
   const int QT = (Q + RX - 1) / RX, PT = (P + RY - 1) / RY, ntiles = PT * QT;
 
