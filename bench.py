@@ -46,7 +46,8 @@ def bench_workload(name: str):
 
 
 def build_inputs(blocks, per_block: int, seed0: int) -> Batch:
-    return Batch.concat([w.batch(B=per_block, seed0=seed0) for w in blocks])
+    workers = min(32, os.cpu_count() or 1)
+    return Batch.concat([w.batch(B=per_block, seed0=seed0, workers=workers) for w in blocks])
 
 
 def flops_per_unit(w) -> float:
@@ -128,18 +129,20 @@ def cpu_sample_indices(B_block: int, n_blocks: int, n: int):
 
 
 def cpu_time(blocks, batch: Batch, per_block: int, target_s: float, pool):
+    """Rounds of `workers` realizations (one per process) until >= target_s of
+    wall time; returns realizations / second over all rounds."""
     from oracle.cpu_baseline import tasks_from_batch, time_tasks
 
     w = blocks[0]
     opts = dict(eps1=w.eps1, eps2=w.eps2, max_iters=w.max_iters)
-    # size the sample: time one round of `workers` realizations, scale to target
-    probe_idx = cpu_sample_indices(per_block, len(blocks), pool.workers)
-    t_probe, _ = time_tasks(pool, tasks_from_batch(batch, probe_idx, opts))
-    rounds = max(1, int(target_s / max(t_probe, 1e-3)))
-    n = min(pool.workers * rounds, batch.B)
-    idx = cpu_sample_indices(per_block, len(blocks), n)
-    t, out = time_tasks(pool, tasks_from_batch(batch, idx, opts))
-    iters = sum(o[1] for o in out)
+    order = cpu_sample_indices(per_block, len(blocks), batch.B)
+    n = t = iters = 0
+    while t < target_s and n < batch.B:
+        idx = order[n:n + pool.workers]
+        dt, out = time_tasks(pool, tasks_from_batch(batch, idx, opts))
+        n += len(idx)
+        t += dt
+        iters += sum(o[1] for o in out)
     return dict(value=n / t, seconds=t, n=n, iters=iters)
 
 

@@ -19,12 +19,15 @@ the same complex64 V0).
 
 from __future__ import annotations
 
+import math
+import os
+from concurrent.futures import ProcessPoolExecutor
+
 from dataclasses import dataclass
 
 import numpy as np
 
-from .model import (ALPHA_STREAM, BETA_STREAM, SystemConfig, generate_channels, init_precoders,
-                    philox)
+from .model import ALPHA_STREAM, BETA_STREAM, CHANNEL_STREAM, INIT_STREAM, philox
 
 
 @dataclass
@@ -70,24 +73,63 @@ def kronecker_root(M: int, rho: float = 0.5) -> np.ndarray:
 def build_batch(M: int, N: int, K: int, d: int, B: int, *, p_max: float, sigma2: float = 1.0,
                 weights: str = "ones", channel: str = "iid", dtype=np.complex64,
                 seed0: int = 0) -> Batch:
-    """Batch of B realizations, seeds seed0 .. seed0+B-1."""
-    H = np.empty((B, K, N, M), dtype=dtype)
-    V0 = np.empty((B, K, M, d), dtype=dtype)
-    W = np.empty((B, K), dtype=np.float64)
+    """Batch of B realizations, seeds seed0 .. seed0+B-1.
+
+    Per realization the Philox draws are exactly those of generate_channels /
+    init_precoders (model.py); the Kronecker product, the power projection and
+    the rounding are applied batch-wise (same arithmetic per element)."""
+    rt = np.sqrt(0.5)
+    Hc = np.empty((B, K, N, M), dtype=np.complex128)
+    Vc = np.empty((B, K, M, d), dtype=np.complex128)
+    W = np.ones((B, K), dtype=np.float64)
+    beta = np.empty((B, K)) if channel == "kronecker" else None
+    if channel not in ("iid", "kronecker"):
+        raise ValueError(f"unknown channel model {channel!r}")
     root = kronecker_root(M) if channel == "kronecker" else None
     for b in range(B):
         r = seed0 + b
-        cfg = SystemConfig(M=M, N=N, K=K, d=d, p_max=p_max, channel_seed=r, init_seed=r)
-        h = generate_channels(cfg).channels
-        if channel == "kronecker":
-            beta = 10.0 ** philox(r, BETA_STREAM).uniform(-2.0, 0.0, size=K)
-            h = np.sqrt(beta)[:, None, None] * (h @ root)
-        elif channel != "iid":
-            raise ValueError(f"unknown channel model {channel!r}")
-        H[b] = h
-        V0[b] = init_precoders(cfg).precoders
-        W[b] = uniform_weights(r, K) if weights == "uniform" else 1.0
-    return Batch(H, np.full(B, float(sigma2)), np.full(B, float(p_max)), W, V0)
+        g = philox(r, CHANNEL_STREAM)
+        re = g.standard_normal((K, N, M))
+        im = g.standard_normal((K, N, M))
+        Hc[b] = (re + 1j * im) * rt
+        g = philox(r, INIT_STREAM)
+        re = g.standard_normal((K, M, d))
+        im = g.standard_normal((K, M, d))
+        v = (re + 1j * im) * rt
+        power = float(np.real(np.vdot(v, v)))  # project_sum_power (solvers.py:257-263)
+        Vc[b] = v if power <= p_max else v * math.sqrt(p_max / power)
+        if beta is not None:  # H_k = sqrt(beta_k) G_k R^{1/2}, per realization
+            beta[b] = 10.0 ** philox(r, BETA_STREAM).uniform(-2.0, 0.0, size=K)
+            Hc[b] = np.sqrt(beta[b])[:, None, None] * (Hc[b] @ root)
+        if weights == "uniform":
+            W[b] = uniform_weights(r, K)
+    return Batch(Hc.astype(dtype), np.full(B, float(sigma2)), np.full(B, float(p_max)), W,
+                 Vc.astype(dtype))
+
+
+def _build_chunk(args):
+    from threadpoolctl import threadpool_limits
+
+    kw, seed0, B = args
+    with threadpool_limits(1):  # one BLAS thread per worker process
+        return build_batch(B=B, seed0=seed0, **kw)
+
+
+def build_batch_parallel(M: int, N: int, K: int, d: int, B: int, *, workers: int | None = None,
+                         seed0: int = 0, **kw) -> Batch:
+    """build_batch over a process pool (chunks of consecutive seeds); identical
+    output to build_batch."""
+    workers = workers or os.cpu_count() or 1
+    if workers <= 1 or B < 64:
+        return build_batch(M, N, K, d, B, seed0=seed0, **kw)
+    chunk = -(-B // (4 * workers))
+    jobs = [(dict(M=M, N=N, K=K, d=d, **kw), seed0 + s, min(chunk, B - s))
+            for s in range(0, B, chunk)]
+    with ProcessPoolExecutor(max_workers=workers) as pool:
+        parts = list(pool.map(_build_chunk, jobs))
+    cat = lambda f: np.concatenate([getattr(p, f) for p in parts])
+    return Batch(cat("channels"), cat("noise_power"), cat("p_max"), cat("weights"),
+                 cat("init_precoders"))
 
 
 # Named workloads of BASELINE.json "configs" (index in brackets) with the
@@ -114,10 +156,10 @@ class Workload:
     eps1: float = 0.1
     snr_db: float = 20.0
 
-    def batch(self, B: int | None = None, seed0: int = 0) -> Batch:
-        b = build_batch(self.M, self.N, self.K, self.d, self.B if B is None else B,
-                        p_max=self.p_max, weights=self.weights, channel=self.channel,
-                        dtype=self.dtype, seed0=seed0)
+    def batch(self, B: int | None = None, seed0: int = 0, workers: int = 1) -> Batch:
+        b = build_batch_parallel(self.M, self.N, self.K, self.d, self.B if B is None else B,
+                                 p_max=self.p_max, weights=self.weights, channel=self.channel,
+                                 dtype=self.dtype, seed0=seed0, workers=workers)
         b.gamma = np.full(b.B, self.gamma)
         b.omega = np.full(b.B, self.omega)
         return b
