@@ -177,7 +177,7 @@ struct CLayout {
     KN = K * NN;
     KD = K * DD;
     ncol = KL * DD;
-    ldh = M | 1;
+    ldh = ((M + 3) & ~3) + 4;
     ldv = ncol;
     ldg = ncol;
     nV = (size_t)M * ldv;
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
                                 pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
                               };
     if (hres)
-      cgemm_smem<R, 2, 2, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
+      cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
     else
       cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, true>(M, ncol, KN, Hcur, M, stage, L.SB,
                                                               Gr[ysrc], Gi[ysrc], ldg, epi);
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
       gi[p * ldg + q] = ci;
     };
     if (hres)
-      cgemm_smem<R, 2, 2, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
+      cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
     else
       cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, false>(KN, ncol, M, Hcur, M, stage, L.SB,
                                                                Vr[src], Vi[src], ldv, epi);

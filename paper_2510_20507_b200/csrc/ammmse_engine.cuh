@@ -96,9 +96,9 @@ struct Layout {
     K = K_;
     KN = K * NN;
     KD = K * DD;
-    // odd leading dimension for H: GEMM-B reads H down a column of k-steps
-    // from several rows at once; an odd stride spreads them over banks
-    ldh = M | 1;
+    // H rows 16-byte aligned (128-bit loads) and padded by 4 elements so
+    // consecutive rows start 4 banks apart
+    ldh = ((M + 3) & ~3) + 4;
     ldv = KD;
     ldg = KD;
     nH = (size_t)KN * ldh;
@@ -223,6 +223,148 @@ __device__ __forceinline__ void cgemm_smem(int P, int Q, int KD, const R* __rest
 #pragma unroll
       for (int j = 0; j < RX; ++j)
         if (p0 + i < P && q0 + j < Q) epi(p0 + i, q0 + j, cr[i][j], ci[i][j]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised shared-memory complex GEMM (same contract as cgemm_smem).
+// Planar operands are read with 128-bit loads: A runs of RY (CONJT, along p)
+// or KU (!CONJT, along k), B runs of RX along q.  The K loop is split S ways
+// over adjacent lanes; partials are reduced with xor-shuffles, so each tile
+// costs one shuffle round per split level instead of a shared-memory pass.
+// Preconditions (checked by cgemm_ok): P % RY, Q % RX, KD % (S*KU) == 0;
+// lda, ldb, the plane bases and q/p offsets 16-byte aligned; tiles*S <= blockDim.
+// ---------------------------------------------------------------------------
+template <typename R>
+struct V16;
+template <>
+struct V16<float> {
+  using T = float4;
+  static constexpr int n = 4;
+};
+template <>
+struct V16<double> {
+  using T = double2;
+  static constexpr int n = 2;
+};
+template <typename R, int W>
+__device__ __forceinline__ void vload(R (&dst)[W], const R* src) {
+  using VT = typename V16<R>::T;
+  constexpr int n = V16<R>::n;
+  static_assert(W % n == 0, "vector width");
+#pragma unroll
+  for (int v = 0; v < W / n; ++v) {
+    const VT x = reinterpret_cast<const VT*>(src)[v];
+    if constexpr (n == 4) {
+      dst[4 * v] = x.x; dst[4 * v + 1] = x.y; dst[4 * v + 2] = x.z; dst[4 * v + 3] = x.w;
+    } else {
+      dst[2 * v] = x.x; dst[2 * v + 1] = x.y;
+    }
+  }
+}
+
+template <typename R, int RY, int RX, int KU>
+__host__ __device__ inline bool cgemm_ok(int P, int Q, int KD, int lda, int ldb, int S, int threads) {
+  constexpr int n = 16 / (int)sizeof(R);
+  if (P % RY || Q % RX || KD % (S * KU)) return false;
+  if (lda % n || ldb % n) return false;
+  if ((P / RY) * (Q / RX) * S > threads) return false;
+  return true;
+}
+
+// split S that fills the block: largest power of two <= 8 with tiles*S <= threads
+__host__ __device__ inline int pick_split(int tiles, int threads, int KD, int KU) {
+  int S = 1;
+  while (S < 8 && tiles * S * 2 <= threads && KD % (S * 2 * KU) == 0) S *= 2;
+  return S;
+}
+
+template <typename R, int RY, int RX, int KU, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R* __restrict__ Ar,
+                                           const R* __restrict__ Ai, int lda,
+                                           const R* __restrict__ Br, const R* __restrict__ Bi,
+                                           int ldb, Epi epi) {
+  const int QT = Q / RX, tiles = (P / RY) * QT;
+  const int w = threadIdx.x;
+  const bool active = w < tiles * S;
+  const int tile = active ? w / S : 0, s = w - (w / S) * S;
+  const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
+  const int kper = KD / S, kb = s * kper;
+  R cr[RY][RX], ci[RY][RX];
+#pragma unroll
+  for (int i = 0; i < RY; ++i)
+#pragma unroll
+    for (int j = 0; j < RX; ++j) cr[i][j] = ci[i][j] = R(0);
+  if (active) {
+    for (int k = kb; k < kb + kper; k += KU) {
+      R ar[KU][RY], ai[KU][RY];
+      if constexpr (CONJT) {
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+          vload<R, RY>(ar[u], Ar + (k + u) * lda + p0);
+          vload<R, RY>(ai[u], Ai + (k + u) * lda + p0);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < RY; ++i) {
+          R tr[KU], ti[KU];
+          vload<R, KU>(tr, Ar + (p0 + i) * lda + k);
+          vload<R, KU>(ti, Ai + (p0 + i) * lda + k);
+#pragma unroll
+          for (int u = 0; u < KU; ++u) { ar[u][i] = tr[u]; ai[u][i] = ti[u]; }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        R br[RX], bi[RX];
+        vload<R, RX>(br, Br + (k + u) * ldb + q0);
+        vload<R, RX>(bi, Bi + (k + u) * ldb + q0);
+#pragma unroll
+        for (int i = 0; i < RY; ++i)
+#pragma unroll
+          for (int j = 0; j < RX; ++j) {
+            if constexpr (CONJT) {
+              cr[i][j] = fma(ar[u][i], br[j], fma(ai[u][i], bi[j], cr[i][j]));
+              ci[i][j] = fma(ar[u][i], bi[j], fma(-ai[u][i], br[j], ci[i][j]));
+            } else {
+              cr[i][j] = fma(ar[u][i], br[j], fma(-ai[u][i], bi[j], cr[i][j]));
+              ci[i][j] = fma(ar[u][i], bi[j], fma(ai[u][i], br[j], ci[i][j]));
+            }
+          }
+      }
+    }
+  }
+  // split-K reduction over the S adjacent lanes of a tile (S | 32, aligned)
+  for (int o = 1; o < S; o <<= 1) {
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j) {
+        cr[i][j] += __shfl_xor_sync(0xffffffffu, cr[i][j], o);
+        ci[i][j] += __shfl_xor_sync(0xffffffffu, ci[i][j], o);
+      }
+  }
+  if (active) {  // lane s of the tile writes rows i = s, s+S, ...
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+      if (i % S == s)
+#pragma unroll
+        for (int j = 0; j < RX; ++j) epi(p0 + i, q0 + j, cr[i][j], ci[i][j]);
+  }
+}
+
+// Dispatch: fast path when the shape allows, generic 2x2 path otherwise.
+template <typename R, int RY, int RX, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_any(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
+                                          const R* Br, const R* Bi, int ldb, Epi epi) {
+  constexpr int KU = 16 / (int)sizeof(R);
+  const int tiles = (P % RY || Q % RX) ? 0 : (P / RY) * (Q / RX);
+  const int S = tiles ? pick_split(tiles, blockDim.x, KD, CONJT ? 1 : KU) : 1;
+  constexpr int KUe = CONJT ? 1 : KU;
+  if (tiles && cgemm_ok<R, RY, RX, KUe>(P, Q, KD, lda, ldb, S, blockDim.x)) {
+    cgemm_fast<R, RY, RX, KUe, CONJT>(P, Q, KD, S, Ar, Ai, lda, Br, Bi, ldb, epi);
+  } else {
+    cgemm_smem<R, 2, 2, CONJT>(P, Q, KD, Ar, Ai, lda, Br, Bi, ldb, epi);
   }
 }
 
@@ -441,7 +583,7 @@ struct Engine {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
     const int ldg = L.ldg;
-    cgemm_smem<R, 2, 2, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
+    cgemm_any<R, 2, 4, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
                                [&](int p, int q, R cr, R ci) {
                                  gr[p * ldg + q] = cr;
                                  gi[p * ldg + q] = ci;
@@ -459,7 +601,7 @@ struct Engine {
     const int ldv = L.ldv;
     const R st = (R)step, om = (R)omega;
     double pw = 0.0;
-    cgemm_smem<R, 2, 2, true>(L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
+    cgemm_any<R, 4, 4, true>(L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
                               [&](int p, int q, R gr, R gi) {
                                 const int o = p * ldv + q;
                                 R vr = vcr[o], vi = vci[o];
