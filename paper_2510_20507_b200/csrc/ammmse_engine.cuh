@@ -121,10 +121,10 @@ struct Layout {
   //   lndetw K
   //   alpha  K
   //   fu fw fv rate  4K
-  //   ustat  K (stored as double)
+  //   ustat, ust2  K each (k1 / wsr per-user status, stored as double)
   //   red    32
   __host__ __device__ size_t dbl_count() const {
-    return (size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + K + K + 4 * K + K + 32;
+    return (size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + K + K + 4 * K + 2 * K + 32;
   }
   __host__ __device__ size_t dbl_bytes() const { return dbl_count() * sizeof(double); }
 };
@@ -425,7 +425,7 @@ struct Engine {
   R *Hr, *Hi, *Vr[2], *Vi[2], *Gr[2], *Gi[2];
   RC<R>*Uf, *Pf, *Df;  // per user N x d, R
   cd *gram, *ucache, *wcache;
-  double *lndetw, *alpha, *fu, *fw, *fv, *rate, *ustat, *red;
+  double *lndetw, *alpha, *fu, *fw, *fv, *rate, *ustat, *ust2, *red;
   L_t L;
 
   __device__ void bind(unsigned char* smem, int M, int K) {
@@ -451,6 +451,7 @@ struct Engine {
     fv = d; d += K;
     rate = d; d += K;
     ustat = d; d += K;
+    ust2 = d; d += K;
     red = d;
   }
 
@@ -521,7 +522,115 @@ struct Engine {
     wsr_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], U, W, lndetw[k], r, f, st);
     rate[k] = r;
     fv[k] = f;
-    ustat[k] = st;
+    ust2[k] = st;
+  }
+
+  // Gram of user k over `ncols` columns of X, computed by one warp (lanes over
+  // columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
+  __device__ void gram_user(int k, const R* __restrict__ Xr, const R* __restrict__ Xi, int ld,
+                            int ncols, int lane) {
+    double sr[NN][NN], si[NN][NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
+    for (int j = lane; j < ncols; j += 32) {
+      double gr[NN], gi[NN];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        gr[a] = (double)Xr[(k * NN + a) * ld + j];
+        gi[a] = (double)Xi[(k * NN + a) * ld + j];
+      }
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
+          if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        sr[a][b] = warp_allsum(sr[a][b]);
+        if (b < a) si[a][b] = warp_allsum(si[a][b]);
+      }
+    if (lane == 0) {
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
+          if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
+        }
+    }
+  }
+
+  // Ŷ row block of user m (rows mN..mN+N-1), in place over the work G, lanes
+  // over columns.
+  __device__ void yhat_user(int m, R* Gwr, R* Gwi, int ldg, int KD, int lane) {
+    for (int j = lane; j < KD; j += 32) {
+      const int b = j / DD, s = j - b * DD;
+      R yr[NN], yi[NN];
+      if (b == m) {
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          const RC<R> v = Df[(m * NN + a) * DD + s];
+          yr[a] = v.r;
+          yi[a] = v.i;
+        }
+      } else {
+        R gr[NN], gi[NN], qr[DD], qi[DD];
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          gr[a] = Gwr[(m * NN + a) * ldg + j];
+          gi[a] = Gwi[(m * NN + a) * ldg + j];
+        }
+#pragma unroll
+        for (int p = 0; p < DD; ++p) {  // q = U_m^H g
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int a = 0; a < NN; ++a) {
+            const RC<R> u = Uf[(m * NN + a) * DD + p];
+            sr = fma(u.r, gr[a], fma(u.i, gi[a], sr));
+            si = fma(u.r, gi[a], fma(-u.i, gr[a], si));
+          }
+          qr[p] = sr;
+          qi[p] = si;
+        }
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {  // y = P_m q
+          R sr = 0, si = 0;
+#pragma unroll
+          for (int p = 0; p < DD; ++p) {
+            const RC<R> pp = Pf[(m * NN + a) * DD + p];
+            sr = fma(pp.r, qr[p], fma(-pp.i, qi[p], sr));
+            si = fma(pp.r, qi[p], fma(pp.i, qr[p], si));
+          }
+          yr[a] = sr;
+          yi[a] = si;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        Gwr[(m * NN + a) * ldg + j] = yr[a];
+        Gwi[(m * NN + a) * ldg + j] = yi[a];
+      }
+    }
+  }
+
+  // Gram(Ĝ) on all warps | receiver / weight / gradient factors with lanes =
+  // users (as few warps as possible: the fp64 per-user code is issued once per
+  // warp) | Ŷ on all threads.  Two block barriers.
+  __device__ void phase_k1_yhat(R* Gwr, R* Gwi, double sigma2, bool weighted, bool want_f) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int K = L.K, KD = L.KD, ldg = L.ldg;
+    for (int k = warp; k < K; k += nw) gram_user(k, Gwr, Gwi, ldg, KD, lane);
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x) k1_user(k, Gwr, Gwi, ldg, sigma2, weighted, want_f);
+    __syncthreads();
+    build_yhat(Gwr, Gwi, ldg, K, KD);
   }
 
   // Ŷ in place over the work G: (m, j) pairs, j fastest.
@@ -578,15 +687,25 @@ struct Engine {
     }
   }
 
-  // GEMM-B: G[dst] = H · V[src]
-  __device__ void gemm_hv(int src, int dst) {
+  // GEMM-B: G[dst] = H · V[src].  With ghat >= 0 the epilogue also writes the
+  // next iteration's extrapolated Ĝ = G + ω (G − G_prev) (solvers.py:380-390,
+  // by linearity) over G[ghat], which holds G_prev = the current G.
+  __device__ void gemm_hv(int src, int dst, int ghat = -1, double omega = 0.0) {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
+    R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
+    R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
+    const R om = (R)omega;
     const int ldg = L.ldg;
     cgemm_any<R, 2, 4, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
                                [&](int p, int q, R cr, R ci) {
-                                 gr[p * ldg + q] = cr;
-                                 gi[p * ldg + q] = ci;
+                                 const int o = p * ldg + q;
+                                 gr[o] = cr;
+                                 gi[o] = ci;
+                                 if (hr) {
+                                   hr[o] = cr + om * (cr - hr[o]);
+                                   hi[o] = ci + om * (ci - hi[o]);
+                                 }
                                });
   }
 
@@ -703,78 +822,37 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
       ctl.step = 2.0 * ctl.gamma;
       if (a.gamma_used) a.gamma_used[r] = ctl.gamma;
     }
-    // initial G = H V0
-    e.gemm_hv(0, 0);
+    // initial G = H V0 into G[0]; Ĝ(1) = G (no extrapolation at t = 1) into G[1]
+    e.gemm_hv(0, 0, 1, 0.0);
     __syncthreads();
 
     // ---------------- main loop (solvers.py:440-505) ----------------
+    // Per iteration: [warp-fused Gram(Ĝ) -> U/W/Ŷ] | GEMM-A + projection |
+    // GEMM-B (+ next Ĝ) | [warp-fused Gram(G) -> rates] | warp-0 reductions and
+    // state machine: 7 block barriers (+2 inside the power reduction).
     for (int t = 1; t <= a.max_iters; ++t) {
       const int cur = ctl.cur, oth = 1 - cur;
-      if (tid == 0) {  // stage test (solvers.py:449-459)
-        int wn;
-        if (ctl.latched) {
-          wn = 1;
-        } else {
-          double rs = INFINITY;
-          if (ctl.nhist >= 2) {
-            const double den = fabs(ctl.wsr_prev);
-            rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
-          }
-          wn = rs <= a.eps1;
-          if (wn) {
-            if (a.latch) ctl.latched = 1;
-            if (ctl.switch_it < 0) ctl.switch_it = t;
-          }
+      // stage test (solvers.py:449-459), evaluated redundantly by every thread
+      // from the shared state; the latch is committed at the end of the iteration
+      bool wn;
+      if (ctl.latched) {
+        wn = true;
+      } else {
+        double rs = INFINITY;
+        if (ctl.nhist >= 2) {
+          const double den = fabs(ctl.wsr_prev);
+          rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
         }
-        ctl.weighted_now = wn;
+        wn = rs <= a.eps1;
       }
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
-      // Ĝ into the work buffer (the G_old slot)
-      {
-        const R om = (R)ctl.omega;
-        R *gcr = e.Gr[cur], *gci = e.Gi[cur], *gwr = e.Gr[oth], *gwi = e.Gi[oth];
-        for (int i = tid; i < KN * KD; i += blockDim.x) {
-          const int row = i / KD, col = i - row * KD, o = row * ldg + col;
-          R xr = gcr[o], xi = gci[o];
-          if (extrap) {
-            xr = xr + om * (xr - gwr[o]);
-            xi = xi + om * (xi - gwi[o]);
-          }
-          gwr[o] = xr;
-          gwi[o] = xi;
-        }
-      }
+      e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, wn, true);
       __syncthreads();
-      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
-      __syncthreads();
-      const bool weighted = ctl.weighted_now;
-      for (int k = tid; k < K; k += blockDim.x)
-        e.k1_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, weighted, true);
-      __syncthreads();
-      if (tid == 0) {
-        double su = 0.0, sw = 0.0;
-        int st = 0;
-        for (int k = 0; k < K; ++k) {
-          su += e.fu[k];
-          sw += e.fw[k];
-          if (st == 0 && e.ustat[k] != 0.0) st = (int)e.ustat[k];
-        }
-        ctl.f_u = su;
-        ctl.f_w = sw;
-        if (st) {
-          ctl.status = st;
-          ctl.stop = 1;
-        }
-      }
-      __syncthreads();
-      if (ctl.stop) break;
-      e.build_yhat(e.Gr[oth], e.Gi[oth], ldg, K, KD);
-      __syncthreads();
-      // X = V̂ − γ ∇ into V[oth], power
+      // X = V̂ − γ ∇ into V[oth], ‖X‖², projection (solvers.py:358-377, :257-263)
       const double power = e.gemm_grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
       const double pmax = ctl.pmax;
       double scale = 1.0;
-      if (!(power <= pmax)) scale = sqrt(pmax / power);  // project_sum_power (solvers.py:257-263)
+      if (!(power <= pmax)) scale = sqrt(pmax / power);
       if (scale != 1.0) {
         const R sc = (R)scale;
         R *xr = e.Vr[oth], *xi = e.Vi[oth];
@@ -785,61 +863,97 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
         }
       }
       __syncthreads();
-      e.gemm_hv(oth, oth);  // G_new = H V_new (Ŷ is dead)
+      // G_new = H V_new over Ŷ; next Ĝ over G_cur (which becomes G_old)
+      e.gemm_hv(oth, oth, cur, ctl.omega);
       __syncthreads();
-      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
+      {  // Gram(G_new) on all warps
+        const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+        for (int k = warp; k < K; k += nw) e.gram_user(k, e.Gr[oth], e.Gi[oth], ldg, KD, lane);
+      }
       __syncthreads();
-      for (int k = tid; k < K; k += blockDim.x) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
-      __syncthreads();
-      if (tid == 0) {
-        double wsr = 0.0, sv = 0.0;
-        int st = 0;
-        for (int k = 0; k < K; ++k) {
-          wsr += e.rate[k];
+      if (K > 32) {
+        for (int k = tid; k < K; k += blockDim.x) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
+        __syncthreads();
+      }
+      if (tid < 32) {  // warp 0: rates (lanes = users), reductions, state machine
+        const int lane = tid;
+        if (K <= 32) {
+          if (lane < K) e.wsr_user(lane, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
+          __syncwarp();
+        }
+        double su = 0.0, sw = 0.0, sr = 0.0, sv = 0.0;
+        int f1 = K, f2 = K;  // first user with a nonzero status (k1 / wsr)
+        for (int k = lane; k < K; k += 32) {
+          su += e.fu[k];
+          sw += e.fw[k];
+          sr += e.rate[k];
           sv += e.fv[k];
-          if (st == 0 && e.ustat[k] != 0.0) st = (int)e.ustat[k];
+          if (f1 == K && e.ustat[k] != 0.0) f1 = k;
+          if (f2 == K && e.ust2[k] != 0.0) f2 = k;
         }
-        const double total_power = scale == 1.0 ? power : power * scale * scale;
-        if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
-        double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
-        if (t > 1) {
-          const double den = fabs(ctl.wsr_last);
-          rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
-        }
-        ctl.wsr_prev = ctl.wsr_last;
-        ctl.wsr_last = wsr;
-        ctl.nhist += 1;
-        ctl.iters = t;
-        ctl.wsr = wsr;
-        ctl.f_v = sv;
-        ctl.last_weighted = ctl.weighted_now;
-        if (a.trace) {
-          double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
-          tr[AMMMSE_TRACE_T] = (double)t;
-          tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
-          tr[AMMMSE_TRACE_F_VALUE] = sv;
-          tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
-          tr[AMMMSE_TRACE_STAGE] = (double)ctl.weighted_now;
-          tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
-          tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
-          tr[AMMMSE_TRACE_F_AFTER_V] = sv;
-          tr[AMMMSE_TRACE_REL_CHANGE] = rel;
-        }
-        // divergence detector (solvers.py:490-500)
-        ctl.running_max = fmax(ctl.running_max, wsr);
-        if (wsr < 0.5 * ctl.running_max)
-          ctl.drop_streak += 1;
-        else
-          ctl.drop_streak = 0;
-        if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
-        if (st) {
-          ctl.status = st;
-          ctl.stop = 1;
-        } else {
-          ctl.cur = oth;  // shift (solvers.py:502)
-          if (ctl.weighted_now && rel <= a.eps2) {  // stop test (:503-505)
-            ctl.converged = 1;
+        su = warp_allsum(su);
+        sw = warp_allsum(sw);
+        sr = warp_allsum(sr);
+        sv = warp_allsum(sv);
+        f1 = __reduce_min_sync(0xffffffffu, f1);
+        f2 = __reduce_min_sync(0xffffffffu, f2);
+        if (lane == 0) {
+          if (!ctl.latched && wn) {
+            if (a.latch) ctl.latched = 1;
+            if (ctl.switch_it < 0) ctl.switch_it = t;
+          }
+          ctl.f_u = su;
+          ctl.f_w = sw;
+          if (f1 < K) {  // update_weight_matrices raised inside iteration t
+            ctl.status = (int)e.ustat[f1];
             ctl.stop = 1;
+          } else {
+            const double wsr = sr;
+            int st = f2 < K ? (int)e.ust2[f2] : 0;
+            const double total_power = scale == 1.0 ? power : power * scale * scale;
+            if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
+            double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
+            if (t > 1) {
+              const double den = fabs(ctl.wsr_last);
+              rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
+            }
+            ctl.wsr_prev = ctl.wsr_last;
+            ctl.wsr_last = wsr;
+            ctl.nhist += 1;
+            ctl.iters = t;
+            ctl.wsr = wsr;
+            ctl.f_v = sv;
+            ctl.weighted_now = wn;
+            ctl.last_weighted = wn;
+            if (a.trace) {
+              double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
+              tr[AMMMSE_TRACE_T] = (double)t;
+              tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
+              tr[AMMMSE_TRACE_F_VALUE] = sv;
+              tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
+              tr[AMMMSE_TRACE_STAGE] = wn ? 1.0 : 0.0;
+              tr[AMMMSE_TRACE_F_AFTER_U] = su;
+              tr[AMMMSE_TRACE_F_AFTER_W] = sw;
+              tr[AMMMSE_TRACE_F_AFTER_V] = sv;
+              tr[AMMMSE_TRACE_REL_CHANGE] = rel;
+            }
+            // divergence detector (solvers.py:490-500)
+            ctl.running_max = fmax(ctl.running_max, wsr);
+            if (wsr < 0.5 * ctl.running_max)
+              ctl.drop_streak += 1;
+            else
+              ctl.drop_streak = 0;
+            if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
+            if (st) {
+              ctl.status = st;
+              ctl.stop = 1;
+            } else {
+              ctl.cur = oth;  // shift (solvers.py:502)
+              if (wn && rel <= a.eps2) {  // stop test (:503-505)
+                ctl.converged = 1;
+                ctl.stop = 1;
+              }
+            }
           }
         }
       }
@@ -858,10 +972,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
         e.Gi[oth][o] = e.Gi[cur][o];
       }
       __syncthreads();
-      user_grams<R, NN>(e.Gr[oth], e.Gi[oth], ldg, KD, K, e.gram);
-      __syncthreads();
-      for (int k = tid; k < K; k += blockDim.x)
-        e.k1_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, weighted, false);
+      e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, weighted, false);
       __syncthreads();
       if (tid == 0) {
         int st = 0;
@@ -871,8 +982,6 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
       }
       __syncthreads();
       if (ctl.status == 0) {
-        e.build_yhat(e.Gr[oth], e.Gi[oth], ldg, K, KD);
-        __syncthreads();
         const double power = e.gemm_grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false);
         double scale = 1.0;
         if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
