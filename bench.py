@@ -45,8 +45,8 @@ def bench_workload(name: str):
     return [WORKLOADS[name]], name
 
 
-def build_inputs(blocks, per_block: int, seed0: int) -> Batch:
-    workers = min(32, os.cpu_count() or 1)
+def build_inputs(blocks, per_block: int, seed0: int, workers: int = 0) -> Batch:
+    workers = workers or min(32, os.cpu_count() or 1)
     return Batch.concat([w.batch(B=per_block, seed0=seed0, workers=workers) for w in blocks])
 
 
@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gen-workers", type=int, default=0,
+                    help="processes for host input generation (1 under ncu)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -221,7 +223,7 @@ def main():
     blocks, label = bench_workload(args.config)
     w = blocks[0]
     per_block = args.per_block or w.B
-    batch = build_inputs(blocks, per_block, seed0=rank * per_block)
+    batch = build_inputs(blocks, per_block, seed0=rank * per_block, workers=args.gen_workers)
     B = batch.B
     itemsize = np.dtype(w.dtype).itemsize // 2
     eng = AmmmseEngine(dev)

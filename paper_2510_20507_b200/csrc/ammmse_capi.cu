@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "ammmse.h"
@@ -268,12 +269,32 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.B = dims->batch;
   a.hres = plan.cluster ? plan.hres : 1;
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
+  // debug: per-phase clock totals (AMMMSE_PROFILE_PHASES=1), printed to stderr
+  static unsigned long long* prof_buf = nullptr;
+  const char* pe = getenv("AMMMSE_PROFILE_PHASES");
+  const bool profile = pe && pe[0] == '1';
+  if (profile) {
+    if (!prof_buf) cudaMalloc(&prof_buf, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof_buf, 0, 16 * sizeof(unsigned long long), s);
+    a.prof = prof_buf;
+  }
   void* args[] = {&a};
   if (plan.cluster)
     ce = cudaLaunchKernelExC(&cfg, func, args);
   else
     ce = cudaLaunchKernel(func, dim3((unsigned)grid), dim3(threads), args, smem, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "kernel launch (solve)");
+  if (profile) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double tot = 0;
+    for (int i = 0; i < 10; ++i) tot += (double)h[i];
+    fprintf(stderr, "[ammmse phases] engine=%s C=%d hres=%d:", plan.cluster ? "cluster" : "single",
+            plan.cluster, plan.hres);
+    for (int i = 0; i < 10; ++i) fprintf(stderr, " p%d=%.1f%%", i, tot > 0 ? 100.0 * h[i] / tot : 0.0);
+    fprintf(stderr, " (total %.3g CTA-cycles)\n", tot);
+  }
   return AMMMSE_OK;
 }
 

@@ -156,6 +156,150 @@ __device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-stage streamed GEMM (v2).  One RY x RX register tile per thread for the
+// whole K loop (tiles <= blockDim), H chunks staged through NST ring buffers
+// (cp.async, NST-1 chunks in flight), one barrier per chunk, 128-bit loads for
+// B (planar, along q) and for A (interleaved complex runs along p (CONJT) or k).
+//   CONJT : chunk = H rows [k0, k0+KC)     staged [kk][p]   (lds = P)
+//   !CONJT: chunk = H cols [k0, k0+KC)     staged [p][kk]   (lds = KC + 2, rows
+//           144 B apart for KC = 16 so neighbouring rows hit different banks)
+// Preconditions (stream2_ok): P % RY == Q % RX == 0, tiles <= blockDim, Q % 4,
+// ldb % 4 == 0 (float), P*(KC+2) <= SB etc.
+// ---------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ int stream2_kc(bool conjt, int P, int SB) {
+  constexpr int EPC = 16 / sizeof(RC<R>);
+  if (conjt) return SB / P;
+  int kc = 16;
+  while (kc > EPC && P * (kc + EPC) > SB) kc >>= 1;
+  return kc;
+}
+
+template <typename R, int RY, int RX, bool CONJT>
+__host__ __device__ inline bool stream2_ok(int P, int Q, int KD, int ldb, int SB, int threads) {
+  constexpr int n = 16 / (int)sizeof(R);
+  constexpr int EPC = 16 / (int)sizeof(RC<R>);
+  if (sizeof(R) != 4) return false;  // 128-bit A loads pair two complex64 values
+  if (P % RY || Q % RX || RX % n || ldb % n || KD % 2 || RY % 2) return false;
+  if ((P / RY) * (Q / RX) > threads) return false;
+  if (CONJT) {
+    if (SB / P < 1 || P % EPC || (RY * (int)sizeof(RC<R>)) % 16) return false;
+  } else {
+    if (P * (2 * EPC) > SB) return false;
+  }
+  return true;
+}
+
+template <typename R, int RY, int RX, int NST, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>* __restrict__ Hg,
+                                              int ldH, RC<R>* __restrict__ stage, int SB,
+                                              const R* __restrict__ Br, const R* __restrict__ Bi,
+                                              int ldb, Epi epi) {
+  constexpr int EPC = 16 / sizeof(RC<R>);  // complex per 16-byte piece
+  const int KC = stream2_kc<R>(CONJT, P, SB);
+  const int lds = CONJT ? P : KC + EPC;
+  const int nchunks = (KD + KC - 1) / KC;
+  const int QT = Q / RX, ntiles = (P / RY) * QT;
+  const bool active = threadIdx.x < ntiles;
+  const int tile = active ? threadIdx.x : 0;
+  const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
+
+  auto issue = [&](int c) {
+    if (c < nchunks) {
+      const int k0 = c * KC, kc = min(KC, KD - k0);
+      RC<R>* dst = stage + (size_t)(c % NST) * SB;
+      if (CONJT) {
+        const RC<R>* src = Hg + (size_t)k0 * ldH;
+        const int pieces = (kc * P) / EPC;
+        for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
+          const int e = i * EPC, row = e / P, col = e - row * P;
+          cp_async16(dst + row * lds + col, src + (size_t)row * ldH + col);
+        }
+      } else {
+        const int ppr = (kc + EPC - 1) / EPC;
+        for (int i = threadIdx.x; i < P * ppr; i += blockDim.x) {
+          const int row = i / ppr, e = (i - row * ppr) * EPC;
+          cp_async16(dst + row * lds + e, Hg + (size_t)row * ldH + k0 + e);
+        }
+      }
+    }
+    cp_async_commit();  // (possibly empty) group keeps the wait count uniform
+  };
+
+  R cr[RY][RX], ci[RY][RX];
+#pragma unroll
+  for (int i = 0; i < RY; ++i)
+#pragma unroll
+    for (int j = 0; j < RX; ++j) cr[i][j] = ci[i][j] = R(0);
+
+#pragma unroll
+  for (int c = 0; c < NST - 1; ++c) issue(c);
+  for (int c = 0; c < nchunks; ++c) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NST - 2) : "memory");
+    __syncthreads();          // chunk c visible; buffer (c-1) % NST free
+    issue(c + NST - 1);
+    const RC<R>* A = stage + (size_t)(c % NST) * SB;
+    const int k0 = c * KC, kc = min(KC, KD - k0);
+    if (active) {
+      // k-steps in pairs: 128-bit loads of two complex A values per load and
+      // both B rows issued before the 2 x RY x RX x 4 FMAs (latency overlap)
+#pragma unroll 2
+      for (int kk = 0; kk < kc; kk += 2) {
+        R ar[2][RY], ai[2][RY], br[2][RX], bi[2][RX];
+        if constexpr (CONJT) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const RC<R>* a = A + (kk + u) * lds + p0;
+#pragma unroll
+            for (int i = 0; i < RY; i += 2) {
+              R t[4];
+              vload<R, 4>(t, reinterpret_cast<const R*>(a + i));
+              ar[u][i] = t[0]; ai[u][i] = t[1]; ar[u][i + 1] = t[2]; ai[u][i + 1] = t[3];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < RY; ++i) {
+            R t[4];
+            vload<R, 4>(t, reinterpret_cast<const R*>(A + (p0 + i) * lds + kk));
+            ar[0][i] = t[0]; ai[0][i] = t[1]; ar[1][i] = t[2]; ai[1][i] = t[3];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          vload<R, RX>(br[u], Br + (k0 + kk + u) * ldb + q0);
+          vload<R, RX>(bi[u], Bi + (k0 + kk + u) * ldb + q0);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < RY; ++i)
+#pragma unroll
+            for (int j = 0; j < RX; ++j) {
+              if constexpr (CONJT) {
+                cr[i][j] = fma(ar[u][i], br[u][j], fma(ai[u][i], bi[u][j], cr[i][j]));
+                ci[i][j] = fma(ar[u][i], bi[u][j], fma(-ai[u][i], br[u][j], ci[i][j]));
+              } else {
+                cr[i][j] = fma(ar[u][i], br[u][j], fma(-ai[u][i], bi[u][j], cr[i][j]));
+                ci[i][j] = fma(ar[u][i], bi[u][j], fma(ai[u][i], br[u][j], ci[i][j]));
+              }
+            }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();  // ring free for the next GEMM
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+      for (int j = 0; j < RX; ++j) epi(p0 + i, q0 + j, cr[i][j], ci[i][j]);
+  }
+}
+
+constexpr int kStreamStages = 4;
+
 constexpr int kStreamRY = 4, kStreamRX = 2, kStreamTPT = 4;
 
 template <typename R, int NN, int DD>
@@ -169,7 +313,7 @@ struct CLayout {
 
   __host__ __device__ void init(int M_, int K_, int C_, int hres_ = 1) {
     hres = hres_;
-    SB = 16384 / (int)(2 * sizeof(R));  // 16 KB per staging buffer
+    SB = 20480 / (int)(2 * sizeof(R));  // 20 KB per staging buffer (kStreamStages of them)
     M = M_;
     K = K_;
     C = C_;
@@ -182,9 +326,9 @@ struct CLayout {
     ldg = ncol;
     nV = (size_t)M * ldv;
     nG = (size_t)KN * ldg;
-    // resident: planar H (2 planes of KN x ldh); streamed: 2 buffers of SB interleaved
-    // complex elements = 4 SB reals = 2 "planes" of 2 SB
-    nH = hres ? (size_t)KN * ldh : (size_t)2 * SB;
+    // resident: planar H (2 planes of KN x ldh); streamed: kStreamStages buffers of SB
+    // interleaved complex = 2*kStreamStages*SB reals = 2 "planes" of kStreamStages*SB
+    nH = hres ? (size_t)KN * ldh : (size_t)kStreamStages * SB;
     oH = 0;
     oV0 = oH + 2 * nH;
     oV1 = oV0 + 2 * nV;
@@ -422,6 +566,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
                               };
     if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
+    else if (stream2_ok<R, 4, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
+      cgemm_stream2<R, 4, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
+                                                   Gi[ysrc], ldg, epi);
+    else if (stream2_ok<R, 8, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
+      cgemm_stream2<R, 8, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
+                                                   Gi[ysrc], ldg, epi);
     else
       cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, true>(M, ncol, KN, Hcur, M, stage, L.SB,
                                                               Gr[ysrc], Gi[ysrc], ldg, epi);
@@ -439,11 +589,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
     };
     if (hres)
       cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
+    else if (stream2_ok<R, 2, 4, false>(KN, ncol, M, ldv, L.SB, blockDim.x))
+      cgemm_stream2<R, 2, 4, kStreamStages, false>(KN, ncol, M, Hcur, M, stage, L.SB, Vr[src],
+                                                    Vi[src], ldv, epi);
+    else if (stream2_ok<R, 4, 4, false>(KN, ncol, M, ldv, L.SB, blockDim.x))
+      cgemm_stream2<R, 4, 4, kStreamStages, false>(KN, ncol, M, Hcur, M, stage, L.SB, Vr[src],
+                                                    Vi[src], ldv, epi);
     else
       cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, false>(KN, ncol, M, Hcur, M, stage, L.SB,
                                                                Vr[src], Vi[src], ldv, epi);
   };
 
+  PhaseClock pc;
+  pc.init(a.prof);
   for (;;) {
     if (crank == 0 && tid == 0) s_r = atomicAdd(a.counter, 1ULL);
     cl.sync();
@@ -574,6 +732,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         ctl.weighted_now = wn;
       }
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
+      pc.mark(0);
       {
         const R om = (R)ctl.omega;
         R *gcr = Gr[cur], *gci = Gi[cur], *gwr = Gr[oth], *gwi = Gi[oth];
@@ -590,6 +749,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
       __syncthreads();
       gram_partials(Gr[oth], Gi[oth], 0);
       cl.sync();
+      pc.mark(1);
       k1_phase(oth, ctl.weighted_now, true);
       if (tid == 0) {
         ctl.f_u = xsum(XS_FU);
@@ -601,9 +761,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         }
       }
       __syncthreads();
+      pc.mark(2);
       if (ctl.stop) break;
       build_yhat(oth);
       __syncthreads();
+      pc.mark(3);
       const double power = grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
       double scale = 1.0;
       if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
@@ -615,10 +777,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         }
       }
       __syncthreads();
+      pc.mark(4);
       gemm_hv(oth, oth);
       __syncthreads();
+      pc.mark(5);
       gram_partials(Gr[oth], Gi[oth], 1);
       cl.sync();
+      pc.mark(6);
       for (int kl = tid; kl < KL; kl += blockDim.x) {
         cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
         gram_of(1, kl, Tg);
@@ -654,6 +819,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         xs[XS_FV] = sv;
         xs[XS_ST2] = st;
       }
+      pc.mark(7);
       cl.sync();
       if (tid == 0) {
         const double wsr = xsum(XS_RATE);
@@ -703,6 +869,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
         }
       }
       __syncthreads();
+      pc.mark(8);
       if (ctl.stop) break;
     }
 
@@ -770,7 +937,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
     // all remote reads of this realization's exchange buffers are complete
     // before any CTA starts the next realization (its first writes)
     cl.sync();
+    pc.mark(9);
   }
+  pc.flush();
 }
 
 }  // namespace ammmse

@@ -41,6 +41,9 @@
 namespace ammmse {
 
 constexpr int kMaxThreads = 256;
+#ifndef AMMMSE_MINB
+#define AMMMSE_MINB 3
+#endif
 constexpr int kTraceFields = AMMMSE_TRACE_FIELDS;
 constexpr double kCondLimit = 1e12;  // solvers.py:71
 constexpr double kLn2 = 0.69314718055994530942;
@@ -75,6 +78,7 @@ struct EngineArgs {
   int latch;
   int M, K;
   int hres;  // cluster engine: H resident in SMEM (1) or streamed from global (0)
+  unsigned long long* prof;  // debug: per-phase clock64 totals (nullptr = off)
   long long B;
   unsigned long long* counter;
 };
@@ -127,6 +131,33 @@ struct Layout {
     return (size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + K + K + 4 * K + 2 * K + 32;
   }
   __host__ __device__ size_t dbl_bytes() const { return dbl_count() * sizeof(double); }
+};
+
+// Debug phase timers: thread 0 of every CTA accumulates clock64() deltas per
+// phase and adds them to EngineArgs::prof at exit (AMMMSE_PROFILE_PHASES=1).
+constexpr int kProfPhases = 10;
+struct PhaseClock {
+  unsigned long long* out;
+  long long last;
+  long long acc[kProfPhases];
+  __device__ void init(unsigned long long* o) {
+    out = (threadIdx.x == 0) ? o : nullptr;
+    if (out) {
+      last = clock64();
+      for (int i = 0; i < kProfPhases; ++i) acc[i] = 0;
+    }
+  }
+  __device__ __forceinline__ void mark(int i) {
+    if (out) {
+      const long long now = clock64();
+      acc[i] += now - last;
+      last = now;
+    }
+  }
+  __device__ void flush() {
+    if (out)
+      for (int i = 0; i < kProfPhases; ++i) atomicAdd(out + i, (unsigned long long)acc[i]);
+  }
 };
 
 // Control block of the running realization (static shared memory).
@@ -739,7 +770,7 @@ struct Engine {
 };
 
 template <typename R, int NN, int DD>
-__global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_solve_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1) ammmse_solve_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
@@ -748,6 +779,8 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
   const int tid = threadIdx.x;
   const int M = a.M, K = a.K, KN = K * NN, KD = K * DD;
   const int ldh = e.L.ldh, ldv = e.L.ldv, ldg = e.L.ldg;
+  PhaseClock pc;
+  pc.init(a.prof);
 
   for (;;) {
     if (tid == 0) s_r = atomicAdd(a.counter, 1ULL);
@@ -846,8 +879,10 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
         wn = rs <= a.eps1;
       }
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
+      pc.mark(0);
       e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, wn, true);
       __syncthreads();
+      pc.mark(1);
       // X = V̂ − γ ∇ into V[oth], ‖X‖², projection (solvers.py:358-377, :257-263)
       const double power = e.gemm_grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
       const double pmax = ctl.pmax;
@@ -863,14 +898,17 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
         }
       }
       __syncthreads();
+      pc.mark(2);
       // G_new = H V_new over Ŷ; next Ĝ over G_cur (which becomes G_old)
       e.gemm_hv(oth, oth, cur, ctl.omega);
       __syncthreads();
+      pc.mark(3);
       {  // Gram(G_new) on all warps
         const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
         for (int k = warp; k < K; k += nw) e.gram_user(k, e.Gr[oth], e.Gi[oth], ldg, KD, lane);
       }
       __syncthreads();
+      pc.mark(4);
       if (K > 32) {
         for (int k = tid; k < K; k += blockDim.x) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
         __syncthreads();
@@ -958,6 +996,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
         }
       }
       __syncthreads();
+      pc.mark(5);
       if (ctl.stop) break;
     }
 
@@ -1024,7 +1063,9 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? 3 : 1) ammmse_so
       }
     }
     __syncthreads();
+    pc.mark(6);
   }
+  pc.flush();
 }
 
 // ---------------------------------------------------------------------------
