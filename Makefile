@@ -9,8 +9,12 @@ OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS := include/ammmse.h $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/entries.h
 LIB := paper_2510_20507_b200/libammmse.so
 PROBE := paper_2510_20507_b200/libammmse_probe.so
+TCTEST := paper_2510_20507_b200/libammmse_tctest.so
 
-all: $(LIB) $(PROBE)
+all: $(LIB) $(PROBE) $(TCTEST)
+
+$(TCTEST): $(SRC_DIR)/tools/tc_selftest.cu $(SRC_DIR)/tc_umma.cuh
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -shared -o $@ $<
 
 $(PROBE): $(SRC_DIR)/tools/probe.cu include/ammmse_probe.h
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Iinclude -shared -o $@ $<
@@ -23,6 +27,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 clean:
-	rm -rf build $(LIB) $(PROBE)
+	rm -rf build $(LIB) $(PROBE) $(TCTEST)
 
 .PHONY: all clean
