@@ -172,6 +172,7 @@ struct Ctl {
   int stop, status, converged, iters;
   double f_u, f_w, f_v, wsr;
   double scale, total_power;
+  double vscale[2];  // V[i] holds X_i unscaled; the precoders are vscale[i] * X_i
 };
 
 // ---------------------------------------------------------------------------
@@ -721,16 +722,19 @@ struct Engine {
   // GEMM-B: G[dst] = H · V[src].  With ghat >= 0 the epilogue also writes the
   // next iteration's extrapolated Ĝ = G + ω (G − G_prev) (solvers.py:380-390,
   // by linearity) over G[ghat], which holds G_prev = the current G.
-  __device__ void gemm_hv(int src, int dst, int ghat = -1, double omega = 0.0) {
+  __device__ void gemm_hv(int src, int dst, int ghat = -1, double omega = 0.0,
+                          double vscale = 1.0) {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
     R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
     R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
-    const R om = (R)omega;
+    const R om = (R)omega, sc = (R)vscale;
     const int ldg = L.ldg;
     cgemm_any<R, 2, 4, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
                                [&](int p, int q, R cr, R ci) {
                                  const int o = p * ldg + q;
+                                 cr *= sc;  // G = H (c X) = c (H X): projection applied lazily
+                                 ci *= sc;
                                  gr[o] = cr;
                                  gi[o] = ci;
                                  if (hr) {
@@ -740,24 +744,27 @@ struct Engine {
                                });
   }
 
-  // GEMM-A + projection input: X = V̂ − step · H^H Ŷ into V[dst], returns ‖X‖² (fp64,
-  // block-reduced).  V̂ = Vc + ω (Vc − V[dst]) when extrap, else Vc.
-  __device__ double gemm_grad_step(int ysrc, int vcur, int dst, double step, double omega,
-                                   bool extrap) {
+  // GEMM-A + projection input: X = V̂ − step · H^H Ŷ into V[dst] (unscaled).
+  // V̂ = sc·Xc + ω (sc·Xc − so·Xo) when extrap, else sc·Xc, where V[vcur] = Xc
+  // and V[dst] = Xo hold the unscaled iterates (solvers.py:380-390, :358-377).
+  // Per-warp ‖X‖² partials go to red[warp]; after the caller's barrier every
+  // thread sums them (warp order) -> power, identical in all threads.
+  __device__ void gemm_grad_step(int ysrc, int vcur, int dst, double step, double omega,
+                                 bool extrap, double sc_cur, double sc_old) {
     const R* vcr = Vr[vcur];
     const R* vci = Vi[vcur];
     R* xr = Vr[dst];
     R* xi = Vi[dst];
     const int ldv = L.ldv;
-    const R st = (R)step, om = (R)omega;
+    const R st = (R)step, om = (R)omega, sc = (R)sc_cur, so = (R)sc_old;
     double pw = 0.0;
     cgemm_any<R, 4, 4, true>(L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
                               [&](int p, int q, R gr, R gi) {
                                 const int o = p * ldv + q;
-                                R vr = vcr[o], vi = vci[o];
+                                R vr = sc * vcr[o], vi = sc * vci[o];
                                 if (extrap) {  // cur + ω (cur − prev)   (solvers.py:390)
-                                  vr = vr + om * (vr - xr[o]);
-                                  vi = vi + om * (vi - xi[o]);
+                                  vr = vr + om * (vr - so * xr[o]);
+                                  vi = vi + om * (vi - so * xi[o]);
                                 }
                                 const R x_r = vr - st * gr;
                                 const R x_i = vi - st * gi;
@@ -765,7 +772,14 @@ struct Engine {
                                 xi[o] = x_i;
                                 pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
                               });
-    return block_sum(pw, red);
+    pw = warp_allsum(pw);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
+  }
+  // sum of the per-warp partials (call after a barrier)
+  __device__ double red_total() const {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    return s;
   }
 };
 
@@ -829,6 +843,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
         ctl.converged = 0;
         ctl.iters = 0;
         ctl.f_u = ctl.f_w = ctl.f_v = ctl.wsr = 0.0;
+        ctl.vscale[0] = ctl.vscale[1] = 1.0;
       }
     }
     __syncthreads();
@@ -883,24 +898,18 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, wn, true);
       __syncthreads();
       pc.mark(1);
-      // X = V̂ − γ ∇ into V[oth], ‖X‖², projection (solvers.py:358-377, :257-263)
-      const double power = e.gemm_grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
+      // X = V̂ − γ ∇ into V[oth] (unscaled), ‖X‖² partials (solvers.py:358-377)
+      e.gemm_grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap, ctl.vscale[cur],
+                       ctl.vscale[oth]);
+      __syncthreads();
+      pc.mark(2);
+      // projection (solvers.py:257-263), applied lazily: V_new = scale * X
+      const double power = e.red_total();
       const double pmax = ctl.pmax;
       double scale = 1.0;
       if (!(power <= pmax)) scale = sqrt(pmax / power);
-      if (scale != 1.0) {
-        const R sc = (R)scale;
-        R *xr = e.Vr[oth], *xi = e.Vi[oth];
-        for (int i = tid; i < M * KD; i += blockDim.x) {
-          const int row = i / KD, col = i - row * KD, o = row * ldv + col;
-          xr[o] *= sc;
-          xi[o] *= sc;
-        }
-      }
-      __syncthreads();
-      pc.mark(2);
-      // G_new = H V_new over Ŷ; next Ĝ over G_cur (which becomes G_old)
-      e.gemm_hv(oth, oth, cur, ctl.omega);
+      // G_new = H V_new = scale (H X) over Ŷ; next Ĝ over G_cur (which becomes G_old)
+      e.gemm_hv(oth, oth, cur, ctl.omega, scale);
       __syncthreads();
       pc.mark(3);
       {  // Gram(G_new) on all warps
@@ -961,6 +970,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
             ctl.iters = t;
             ctl.wsr = wsr;
             ctl.f_v = sv;
+            ctl.vscale[oth] = scale;
             ctl.weighted_now = wn;
             ctl.last_weighted = wn;
             if (a.trace) {
@@ -1021,7 +1031,10 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       }
       __syncthreads();
       if (ctl.status == 0) {
-        const double power = e.gemm_grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false);
+        const double vs = ctl.vscale[cur];
+        e.gemm_grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false, vs, 1.0);
+        __syncthreads();
+        const double power = e.red_total();
         double scale = 1.0;
         if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
         double dsum = 0.0, vsum = 0.0;
@@ -1029,14 +1042,16 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
         const R* vi = e.Vi[cur];
         const R* xr = e.Vr[oth];
         const R* xi = e.Vi[oth];
+        const R vsr = (R)vs;
         for (int i = tid; i < M * KD; i += blockDim.x) {
           const int row = i / KD, col = i - row * KD, o = row * ldv + col;
-          const double a_r = (double)vr[o], a_i = (double)vi[o];
+          const double a_r = (double)(vsr * vr[o]), a_i = (double)(vsr * vi[o]);
           const double dr = a_r - (double)((R)(xr[o] * (R)scale));
           const double di = a_i - (double)((R)(xi[o] * (R)scale));
           dsum += dr * dr + di * di;
           vsum += a_r * a_r + a_i * a_i;
         }
+        __syncthreads();  // every thread has read the power partials in red[]
         dsum = block_sum(dsum, e.red);
         vsum = block_sum(vsum, e.red);
         residual = sqrt(dsum) / fmax(1.0, sqrt(fmax(vsum, 0.0)));
@@ -1048,9 +1063,10 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       const int cur = ctl.cur;
       if (a.Vout) {
         RC<R>* Vg = reinterpret_cast<RC<R>*>(a.Vout) + (size_t)r * K * M * DD;
+        const R vs = (R)ctl.vscale[cur];
         for (int i = tid; i < K * M * DD; i += blockDim.x) {
           const int k = i / (M * DD), rem = i - k * M * DD, m = rem / DD, s = rem - m * DD;
-          Vg[i] = RC<R>{e.Vr[cur][m * ldv + k * DD + s], e.Vi[cur][m * ldv + k * DD + s]};
+          Vg[i] = RC<R>{vs * e.Vr[cur][m * ldv + k * DD + s], vs * e.Vi[cur][m * ldv + k * DD + s]};
         }
       }
       if (tid == 0) {
