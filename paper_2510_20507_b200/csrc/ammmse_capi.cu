@@ -99,7 +99,7 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
         p->cluster = c;
         p->hres = hres;
         p->smem = s;
-        p->threads = 256;
+        p->threads = 256;  // kClusterThreads
         return AMMMSE_OK;
       }
     }

@@ -205,22 +205,37 @@ __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>*
   const int tile = active ? threadIdx.x : 0;
   const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
 
+  // per-thread copy cursor: (row, element) of this thread's first 16-byte piece,
+  // advanced incrementally (no integer division in the chunk loop)
+  const int stride_e = blockDim.x * EPC;
   auto issue = [&](int c) {
     if (c < nchunks) {
       const int k0 = c * KC, kc = min(KC, KD - k0);
       RC<R>* dst = stage + (size_t)(c % NST) * SB;
-      if (CONJT) {
+      if (CONJT) {  // kc rows of P elements, contiguous in global and in the stage
         const RC<R>* src = Hg + (size_t)k0 * ldH;
-        const int pieces = (kc * P) / EPC;
-        for (int i = threadIdx.x; i < pieces; i += blockDim.x) {
-          const int e = i * EPC, row = e / P, col = e - row * P;
-          cp_async16(dst + row * lds + col, src + (size_t)row * ldH + col);
+        const int total = kc * P;
+        if (ldH == P) {
+          for (int e = threadIdx.x * EPC; e < total; e += stride_e) cp_async16(dst + e, src + e);
+        } else {
+          int row = (threadIdx.x * EPC) / P, col = threadIdx.x * EPC - row * P;
+          const int drow = stride_e / P, dcol = stride_e - drow * P;
+          for (int e = threadIdx.x * EPC; e < total; e += stride_e) {
+            cp_async16(dst + row * lds + col, src + (size_t)row * ldH + col);
+            row += drow;
+            col += dcol;
+            if (col >= P) { col -= P; ++row; }
+          }
         }
-      } else {
-        const int ppr = (kc + EPC - 1) / EPC;
-        for (int i = threadIdx.x; i < P * ppr; i += blockDim.x) {
-          const int row = i / ppr, e = (i - row * ppr) * EPC;
+      } else {      // P rows, kc elements each (row segments)
+        const int rowlen = ((kc + EPC - 1) / EPC) * EPC;
+        const int drow = stride_e / rowlen, de = stride_e - drow * rowlen;
+        int row = (threadIdx.x * EPC) / rowlen, e = threadIdx.x * EPC - row * rowlen;
+        while (row < P) {
           cp_async16(dst + row * lds + e, Hg + (size_t)row * ldH + k0 + e);
+          row += drow;
+          e += de;
+          if (e >= rowlen) { e -= rowlen; ++row; }
         }
       }
     }
@@ -302,6 +317,11 @@ constexpr int kStreamStages = 4;
 
 constexpr int kStreamRY = 4, kStreamRX = 2, kStreamTPT = 4;
 
+// threads per CTA of the cluster engine (512 was measured slower: register cap
+// -> spills in the GEMM loops, half-idle GEMM-B tiles)
+template <int NN, int DD>
+constexpr int kClusterThreads = 256;
+
 template <typename R, int NN, int DD>
 struct CLayout {
   int M, K, C, KL, KN, KD, ncol, ldh, ldv, ldg;
@@ -351,7 +371,7 @@ struct CLayout {
 };
 
 template <typename R, int NN, int DD>
-__global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineArgs a) {
+__global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
@@ -566,6 +586,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) ammmse_cluster_kernel(EngineAr
                               };
     if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
+    else if ((M / 4) * (ncol / 4) < (int)blockDim.x &&
+             stream2_ok<R, 2, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
+      cgemm_stream2<R, 2, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
+                                                   Gi[ysrc], ldg, epi);
     else if (stream2_ok<R, 4, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
       cgemm_stream2<R, 4, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
                                                    Gi[ysrc], ldg, epi);
