@@ -114,7 +114,8 @@ typedef struct AmmmseOptions {
                           engine with c CTAs per realization (c in {1,2,4,8,16}, c | K) —
                           a tuning / testing knob, results are identical up to rounding */
   int32_t h_placement; /* cluster engine only: 0 auto, 1 H resident in every CTA's SMEM,
-                          2 H streamed from HBM/L2 through a cp.async ring */
+                          2 H streamed from HBM/L2 through a cp.async ring, 3 streamed H and
+                          the previous precoders in a per-CTA global scratch slot */
   int32_t reserved;
 } AmmmseOptions;
 

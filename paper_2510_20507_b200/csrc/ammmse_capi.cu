@@ -62,6 +62,8 @@ struct Plan {
   const ammmse::KernelEntry* e;
   int cluster;  // 0: single-CTA engine; >= 1: cluster engine with that many CTAs
   int hres;     // cluster engine: H resident (1) or streamed (0)
+  int vglob;    // cluster engine: V_old in global scratch
+  int sb;       // cluster engine: staging bytes per buffer
   size_t smem;
   int threads;
 };
@@ -74,6 +76,9 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
   int lim = max_smem_optin();
   if (lim <= 0) lim = 232448;  // sm_100 opt-in limit (no device to query)
   p->e = e;
+  p->hres = 1;
+  p->vglob = 0;
+  p->sb = 20480;
   if (force_c == 0 && h_placement == 0) {
     const size_t s1 = e->smem_bytes(d->M, d->K);
     if (s1 <= (size_t)lim) {
@@ -83,10 +88,16 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
       return AMMMSE_OK;
     }
   }
-  // H resident in every CTA of the smallest cluster that fits, else H streamed
+  // In order of preference: H resident in every CTA of the smallest cluster
+  // that fits; H streamed (20 KB staging buffers); H streamed with V_old in a
+  // global scratch slot and smaller staging buffers (M = 512 sweep).
   const int cands[5] = {1, 2, 4, 8, 16};
-  for (int hres = 1; hres >= 0; --hres) {
-    if ((h_placement == 1 && !hres) || (h_placement == 2 && hres)) continue;
+  const int modes[4][3] = {{1, 0, 20480}, {0, 0, 20480}, {0, 1, 20480}, {0, 1, 12288}};
+  for (int mi = 0; mi < 4; ++mi) {
+    const int hres = modes[mi][0], vglob = modes[mi][1], sb = modes[mi][2];
+    if ((h_placement == 1 && !hres) || (h_placement == 2 && (hres || vglob)) ||
+        (h_placement == 3 && (hres || !vglob)))
+      continue;
     for (int i = 0; i < 5; ++i) {
       const int c = cands[i];
       if (force_c && c != force_c) continue;
@@ -94,10 +105,12 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
       if (d->K % c) continue;
       // streamed H moves 16-byte pieces: complex64 rows need an even length
       if (!hres && d->dtype == AMMMSE_COMPLEX64 && (d->M % 2)) continue;
-      const size_t s = e->cluster_smem_bytes(d->M, d->K, c, hres);
+      const size_t s = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb);
       if (s <= (size_t)lim) {
         p->cluster = c;
         p->hres = hres;
+        p->vglob = vglob;
+        p->sb = sb;
         p->smem = s;
         p->threads = 256;  // kClusterThreads
         return AMMMSE_OK;
@@ -124,6 +137,19 @@ int cuda_fail(cudaError_t e, const char* what) {
   return AMMMSE_ERR_CUDA;
 }
 
+// bytes of per-CTA V_old scratch (cluster engine, vglob plans); one CTA per SM
+// is resident for those plans, so the slot count is bounded by the SM count
+size_t scratch_bytes(const AmmmseDims* d, const Plan& p) {
+  if (!p.cluster || !p.vglob) return 0;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    sms = 160;
+  const size_t rsz = d->dtype == AMMMSE_COMPLEX64 ? 4 : 8;
+  const size_t ncol = (size_t)(d->K / p.cluster) * d->d;
+  return (size_t)sms * 2 * (size_t)d->M * ncol * rsz;
+}
+
 }  // namespace
 
 extern "C" {
@@ -139,7 +165,9 @@ int ammmse_check_dims(const AmmmseDims* dims) {
 
 size_t ammmse_workspace_size(const AmmmseDims* dims) {
   if (dims_valid(dims)) return 0;
-  return 256;  // work counter, padded
+  Plan p;
+  if (make_plan(dims, 0, 0, &p) != AMMMSE_OK) return 256;
+  return 256 + scratch_bytes(dims, p);  // work counter (padded) + V_old scratch
 }
 
 int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const AmmmseOptions* opt,
@@ -175,15 +203,19 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     snprintf(g_err, sizeof g_err, "max_iters must be at least 1");
     return AMMMSE_ERR_INVALID;
   }
-  if (!workspace || workspace_bytes < ammmse_workspace_size(dims)) {
+  if (!workspace || workspace_bytes < 256) {
     snprintf(g_err, sizeof g_err, "workspace missing or too small");
     return AMMMSE_ERR_WORKSPACE;
   }
   Plan plan;
-  if (opt->cluster_size < 0 || opt->h_placement < 0 || opt->h_placement > 2 ||
+  if (opt->cluster_size < 0 || opt->h_placement < 0 || opt->h_placement > 3 ||
       make_plan(dims, opt->cluster_size, opt->h_placement, &plan) != AMMMSE_OK) {
     snprintf(g_err, sizeof g_err, "no engine configuration fits (cluster_size %d)", opt->cluster_size);
     return AMMMSE_ERR_UNSUPPORTED;
+  }
+  if (workspace_bytes < 256 + scratch_bytes(dims, plan)) {
+    snprintf(g_err, sizeof g_err, "workspace missing or too small");
+    return AMMMSE_ERR_WORKSPACE;
   }
   const void* func = plan.cluster ? plan.e->cluster_solve : plan.e->solve;
   const size_t smem = plan.smem;
@@ -268,6 +300,9 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.K = dims->K;
   a.B = dims->batch;
   a.hres = plan.cluster ? plan.hres : 1;
+  a.vold_glob = plan.cluster ? plan.vglob : 0;
+  a.sb_bytes = plan.sb;
+  a.scratch = reinterpret_cast<unsigned char*>(workspace) + 256;
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
   // debug: per-phase clock totals (AMMMSE_PROFILE_PHASES=1), printed to stderr
   static unsigned long long* prof_buf = nullptr;

@@ -326,14 +326,17 @@ template <typename R, int NN, int DD>
 struct CLayout {
   int M, K, C, KL, KN, KD, ncol, ldh, ldv, ldg;
   int hres;  // 1: H resident in SMEM;  0: H streamed from global through `stage`
+  int vglob; // 1: the second V buffer lives in a per-CTA global scratch slot (L2)
   int SB;    // staging buffer size (complex elements) when streamed
   size_t nH, nV, nG;
   size_t oH, oV0, oV1, oG0, oG1, oUall, oPall, oDown;  // R offsets (planar / RC)
   size_t dbl_off, bytes;
 
-  __host__ __device__ void init(int M_, int K_, int C_, int hres_ = 1) {
+  __host__ __device__ void init(int M_, int K_, int C_, int hres_ = 1, int vglob_ = 0,
+                                int sb_bytes = 20480) {
     hres = hres_;
-    SB = 20480 / (int)(2 * sizeof(R));  // 20 KB per staging buffer (kStreamStages of them)
+    vglob = vglob_;
+    SB = sb_bytes / (int)(2 * sizeof(R));  // per staging buffer (kStreamStages of them)
     M = M_;
     K = K_;
     C = C_;
@@ -352,7 +355,7 @@ struct CLayout {
     oH = 0;
     oV0 = oH + 2 * nH;
     oV1 = oV0 + 2 * nV;
-    oG0 = oV1 + 2 * nV;
+    oG0 = oV1 + (vglob ? 0 : 2 * nV);
     oG1 = oG0 + 2 * nG;
     oUall = oG1 + 2 * nG;                       // RC<R>[K*NN*DD]
     oPall = oUall + (size_t)2 * K * NN * DD;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   const int tid = threadIdx.x;
 
   CLayout<R, NN, DD> L;
-  L.init(a.M, a.K, C, a.hres);
+  L.init(a.M, a.K, C, a.hres, a.vold_glob, a.sb_bytes);
   const bool hres = a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
@@ -395,7 +398,12 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   const RC<R>* Hcur = nullptr;                            // this realization's H in global
   R *Vr[2], *Vi[2], *Gr[2], *Gi[2];
   Vr[0] = base + L.oV0; Vi[0] = Vr[0] + L.nV;
-  Vr[1] = base + L.oV1; Vi[1] = Vr[1] + L.nV;
+  if (L.vglob) {  // V_old slot in global scratch (generic pointers: every path works)
+    Vr[1] = reinterpret_cast<R*>(a.scratch) + (size_t)blockIdx.x * 2 * L.nV;
+  } else {
+    Vr[1] = base + L.oV1;
+  }
+  Vi[1] = Vr[1] + L.nV;
   Gr[0] = base + L.oG0; Gi[0] = Gr[0] + L.nG;
   Gr[1] = base + L.oG1; Gi[1] = Gr[1] + L.nG;
   RC<R>* Uall = reinterpret_cast<RC<R>*>(base + L.oUall);

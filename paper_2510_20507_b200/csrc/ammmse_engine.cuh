@@ -78,6 +78,9 @@ struct EngineArgs {
   int latch;
   int M, K;
   int hres;  // cluster engine: H resident in SMEM (1) or streamed from global (0)
+  int vold_glob;  // cluster engine: second V buffer in global scratch (1)
+  int sb_bytes;   // cluster engine: bytes per cp.async staging buffer
+  unsigned char* scratch;  // cluster engine: per-CTA global scratch (vold_glob)
   unsigned long long* prof;  // debug: per-phase clock64 totals (nullptr = off)
   long long B;
   unsigned long long* counter;

@@ -185,15 +185,17 @@ def test_cluster_engine_complex64_medium(cuda, csize, hp):
     assert np.array_equal(g.iterations[ok], r["iterations"][ok])
 
 
-@pytest.mark.parametrize("M,N,K,d,csize", [(16, 2, 4, 2, 2), (12, 4, 4, 4, 4), (10, 1, 4, 2, 2)])
-def test_cluster_engine_streamed_h_complex128(cuda, M, N, K, d, csize):
+@pytest.mark.parametrize("M,N,K,d,csize,hp", [(16, 2, 4, 2, 2, 2), (12, 4, 4, 4, 4, 2),
+                                               (10, 1, 4, 2, 2, 2), (16, 2, 4, 2, 2, 3),
+                                               (12, 4, 4, 4, 4, 3)])
+def test_cluster_engine_streamed_h_complex128(cuda, M, N, K, d, csize, hp):
     """Streamed-H cluster mode (H through the cp.async ring), forced on small fp64
     shapes, against the oracle."""
     b = build_batch(M, N, K, d, 3, p_max=50.0, weights="uniform", dtype=np.complex128, seed0=9)
     kw = dict(gamma=0.005, omega=0.7, eps2=1e-6, max_iters=80)
     opts = SolverOptions(algorithm="ammmse", **kw)
     g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
-                         record_trace=True, cluster_size=csize, h_placement=2)
+                         record_trace=True, cluster_size=csize, h_placement=hp)
     r = oracle_solve(b, **kw)
     assert np.array_equal(g.iterations, r["iterations"])
     np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-9)
