@@ -170,7 +170,7 @@ __device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* 
 template <typename R>
 __device__ __forceinline__ int stream2_kc(bool conjt, int P, int SB) {
   constexpr int EPC = 16 / sizeof(RC<R>);
-  if (conjt) return SB / P;
+  if (conjt) return (SB / P) & ~1;  // the k loop consumes k-steps in pairs
   int kc = 16;
   while (kc > EPC && P * (kc + EPC) > SB) kc >>= 1;
   return kc;
@@ -184,7 +184,7 @@ __host__ __device__ inline bool stream2_ok(int P, int Q, int KD, int ldb, int SB
   if (P % RY || Q % RX || RX % n || ldb % n || KD % 2 || RY % 2) return false;
   if ((P / RY) * (Q / RX) > threads) return false;
   if (CONJT) {
-    if (SB / P < 1 || P % EPC || (RY * (int)sizeof(RC<R>)) % 16) return false;
+    if (SB / P < 2 || P % EPC || (RY * (int)sizeof(RC<R>)) % 16) return false;
   } else {
     if (P * (2 * EPC) > SB) return false;
   }

@@ -200,3 +200,17 @@ def test_cluster_engine_streamed_h_complex128(cuda, M, N, K, d, csize, hp):
     assert np.array_equal(g.iterations, r["iterations"])
     np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-9)
     np.testing.assert_allclose(g.final_precoders, r["final_precoders"], rtol=0, atol=1e-8)
+
+
+def test_cluster_streamed_odd_stage_rows_complex64(cuda):
+    """Chunk extents that are not multiples of the k-pair unroll (regression:
+    M = 512 with 12 KB staging gave 3-row chunks)."""
+    b = build_batch(96, 2, 8, 2, 2, p_max=30.0, weights="uniform", dtype=np.complex64, seed0=5)
+    kw = dict(gamma=0.003, omega=0.8, eps2=1e-5, max_iters=60)
+    opts = SolverOptions(algorithm="ammmse", **kw)
+    for hp in (2, 3):
+        g = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                             cluster_size=2, h_placement=hp)
+        r = oracle_solve(b, **kw)
+        rel = np.abs(g.wsr_bits - r["wsr_bits"]) / np.abs(r["wsr_bits"])
+        assert rel.max() <= WSR_RTOL_C64, (hp, rel)
