@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cluster-size", type=int, default=0, help="engine knob (0 = automatic)")
+    ap.add_argument("--h-placement", type=int, default=0, help="engine knob (0 = automatic)")
     ap.add_argument("--gen-workers", type=int, default=0,
                     help="processes for host input generation (1 under ncu)")
     args = ap.parse_args()
@@ -230,7 +232,7 @@ def main():
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     # per-realization (gamma, omega): each SNR block carries its own step
     kw = dict(gamma=to(batch.gamma), omega=to(batch.omega), eps1=w.eps1, eps2=w.eps2,
-              max_iters=w.max_iters)
+              max_iters=w.max_iters, cluster_size=args.cluster_size, h_placement=args.h_placement)
     dH, ds2, dP, dA, dV0 = (to(batch.channels), to(batch.noise_power), to(batch.p_max),
                             to(batch.weights), to(batch.init_precoders))
     stream = torch.cuda.current_stream(dev)

@@ -145,8 +145,13 @@ int ammmse_abi_version(void);
 /* 0 if the dims are supported by the compiled engine, else AMMMSE_ERR_* */
 int ammmse_check_dims(const AmmmseDims* dims);
 
-/* bytes of device workspace ammmse_solve needs (0 on invalid dims) */
+/* bytes of device workspace ammmse_solve needs with automatic engine choice
+   (0 on invalid dims) */
 size_t ammmse_workspace_size(const AmmmseDims* dims);
+
+/* same, for the engine configuration `options` selects (cluster_size /
+   h_placement knobs); 0 if no configuration fits */
+size_t ammmse_workspace_size_opts(const AmmmseDims* dims, const AmmmseOptions* options);
 
 /* Solve all B realizations.  Replaces run_ammmse (solvers.py:540-550). */
 int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* problem,

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "ammmse_abi_version",
     "ammmse_check_dims",
     "ammmse_workspace_size",
+    "ammmse_workspace_size_opts",
     "ammmse_solve",
     "ammmse_bounds",
     "ammmse_error_string",
@@ -91,6 +92,8 @@ def lib() -> ctypes.CDLL:
         h.ammmse_check_dims.argtypes = [ctypes.POINTER(AmmmseDims)]
         h.ammmse_workspace_size.restype = ctypes.c_size_t
         h.ammmse_workspace_size.argtypes = [ctypes.POINTER(AmmmseDims)]
+        h.ammmse_workspace_size_opts.restype = ctypes.c_size_t
+        h.ammmse_workspace_size_opts.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.POINTER(AmmmseOptions)]
         h.ammmse_solve.restype = ctypes.c_int
         h.ammmse_solve.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.POINTER(AmmmseProblem),
                                    ctypes.POINTER(AmmmseOptions), ctypes.POINTER(AmmmseResult),

@@ -325,7 +325,10 @@ class AmmmseEngine:
             ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
             ptr(out.stationarity_residual), ptr(out.switch_iteration), ptr(out.status),
             ptr(out.gamma_used), ptr(out.trace))
-        ws_bytes = int(self.lib.ammmse_workspace_size(dims))
+        ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
+        if ws_bytes == 0:
+            raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
+                              f"h_placement={h_placement})")
         ws = self._workspace(ws_bytes)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
