@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cluster-size", type=int, default=0, help="engine knob (0 = automatic)")
     ap.add_argument("--h-placement", type=int, default=0, help="engine knob (0 = automatic)")
+    ap.add_argument("--tensor-cores", type=int, default=0, help="engine knob (0 auto, 1 on, 2 off)")
     ap.add_argument("--gen-workers", type=int, default=0,
                     help="processes for host input generation (1 under ncu)")
     args = ap.parse_args()
@@ -232,7 +233,8 @@ def main():
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     # per-realization (gamma, omega): each SNR block carries its own step
     kw = dict(gamma=to(batch.gamma), omega=to(batch.omega), eps1=w.eps1, eps2=w.eps2,
-              max_iters=w.max_iters, cluster_size=args.cluster_size, h_placement=args.h_placement)
+              max_iters=w.max_iters, cluster_size=args.cluster_size, h_placement=args.h_placement,
+              tensor_cores=args.tensor_cores)
     dH, ds2, dP, dA, dV0 = (to(batch.channels), to(batch.noise_power), to(batch.p_max),
                             to(batch.weights), to(batch.init_precoders))
     stream = torch.cuda.current_stream(dev)

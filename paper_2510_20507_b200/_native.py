@@ -57,7 +57,7 @@ class AmmmseOptions(ctypes.Structure):
                 ("max_iters", ctypes.c_int32), ("omega", ctypes.c_double),
                 ("eps1", ctypes.c_double), ("eps2", ctypes.c_double),
                 ("latch_stage", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
-                ("h_placement", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("h_placement", ctypes.c_int32), ("tensor_cores", ctypes.c_int32)]
 
 
 class AmmmseResult(ctypes.Structure):

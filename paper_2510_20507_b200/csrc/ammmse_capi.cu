@@ -13,7 +13,7 @@
 #include <string.h>
 
 #include "ammmse.h"
-#include "ammmse_engine.cuh"
+#include "ammmse_cluster.cuh"
 #include "entries.h"
 
 namespace {
@@ -64,13 +64,14 @@ struct Plan {
   int hres;     // cluster engine: H resident (1) or streamed (0)
   int vglob;    // cluster engine: V_old in global scratch
   int sb;       // cluster engine: staging bytes per buffer
+  int tc;       // cluster engine: tcgen05 GEMMs
   size_t smem;
   int threads;
 };
 
 int pick_threads(const AmmmseDims* d);
 
-int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
+int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_cores, Plan* p) {
   const ammmse::KernelEntry* e = lookup(d);
   if (!e) return AMMMSE_ERR_UNSUPPORTED;
   int lim = max_smem_optin();
@@ -79,7 +80,8 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
   p->hres = 1;
   p->vglob = 0;
   p->sb = 20480;
-  if (force_c == 0 && h_placement == 0) {
+  p->tc = 0;
+  if (force_c == 0 && h_placement == 0 && tensor_cores != 1) {
     const size_t s1 = e->smem_bytes(d->M, d->K);
     if (s1 <= (size_t)lim) {
       p->cluster = 0;
@@ -105,7 +107,24 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, Plan* p) {
         continue;
       // streamed H moves 16-byte pieces: complex64 rows need an even length
       if (!hres && d->dtype == AMMMSE_COMPLEX64 && (d->M % 2)) continue;
-      const size_t s = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb);
+      // tensor-core GEMMs (streamed pre-split H planes) when the shape allows
+      const int ncol = (d->K / c) * d->d;
+      if (!hres && d->dtype == AMMMSE_COMPLEX64 && tensor_cores != 2 &&
+          ammmse::tc_shape_ok(d->M, d->K * d->N, ncol)) {
+        const size_t st = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb, 1);
+        if (st <= (size_t)lim) {
+          p->cluster = c;
+          p->hres = hres;
+          p->vglob = vglob;
+          p->sb = sb;
+          p->tc = 1;
+          p->smem = st;
+          p->threads = 256;
+          return AMMMSE_OK;
+        }
+      }
+      if (tensor_cores == 1) continue;
+      const size_t s = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb, 0);
       if (s <= (size_t)lim) {
         p->cluster = c;
         p->hres = hres;
@@ -137,17 +156,27 @@ int cuda_fail(cudaError_t e, const char* what) {
   return AMMMSE_ERR_CUDA;
 }
 
+// tensor-core mode: pre-split H / H^T planes (8 planes of KN x M floats) per
+// resident cluster (one CTA per SM -> at most sms / C clusters), after the
+// V_old slots
+size_t tc_planes_bytes(const AmmmseDims* d, const Plan& p, int sms) {
+  const size_t per = (size_t)8 * d->K * d->N * d->M * 4;
+  return (size_t)((sms + p.cluster - 1) / p.cluster) * per + 256;
+}
+
 // bytes of per-CTA V_old scratch (cluster engine, vglob plans); one CTA per SM
 // is resident for those plans, so the slot count is bounded by the SM count
 size_t scratch_bytes(const AmmmseDims* d, const Plan& p) {
-  if (!p.cluster || !p.vglob) return 0;
+  if (!p.cluster || (!p.vglob && !p.tc)) return 0;
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
     sms = 160;
   const size_t rsz = d->dtype == AMMMSE_COMPLEX64 ? 4 : 8;
   const size_t ncol = (size_t)(d->K / p.cluster) * d->d;
-  return (size_t)sms * 2 * (size_t)d->M * ncol * rsz;
+  size_t b = p.vglob ? (size_t)sms * 2 * (size_t)d->M * ncol * rsz : 0;
+  if (p.tc) b += tc_planes_bytes(d, p, sms);
+  return b;
 }
 
 }  // namespace
@@ -160,20 +189,21 @@ int ammmse_check_dims(const AmmmseDims* dims) {
   int rc = dims_valid(dims);
   if (rc) return rc;
   Plan p;
-  return make_plan(dims, 0, 0, &p);
+  return make_plan(dims, 0, 0, 0, &p);
 }
 
 size_t ammmse_workspace_size(const AmmmseDims* dims) {
   if (dims_valid(dims)) return 0;
   Plan p;
-  if (make_plan(dims, 0, 0, &p) != AMMMSE_OK) return 256;
+  if (make_plan(dims, 0, 0, 0, &p) != AMMMSE_OK) return 256;
   return 256 + scratch_bytes(dims, p);  // work counter (padded) + V_old scratch
 }
 
 size_t ammmse_workspace_size_opts(const AmmmseDims* dims, const AmmmseOptions* opt) {
   if (dims_valid(dims) || !opt) return 0;
   Plan p;
-  if (make_plan(dims, opt->cluster_size, opt->h_placement, &p) != AMMMSE_OK) return 0;
+  if (make_plan(dims, opt->cluster_size, opt->h_placement, opt->tensor_cores, &p) != AMMMSE_OK)
+    return 0;
   return 256 + scratch_bytes(dims, p);
 }
 
@@ -216,7 +246,8 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   }
   Plan plan;
   if (opt->cluster_size < 0 || opt->h_placement < 0 || opt->h_placement > 3 ||
-      make_plan(dims, opt->cluster_size, opt->h_placement, &plan) != AMMMSE_OK) {
+      opt->tensor_cores < 0 || opt->tensor_cores > 2 ||
+      make_plan(dims, opt->cluster_size, opt->h_placement, opt->tensor_cores, &plan) != AMMMSE_OK) {
     snprintf(g_err, sizeof g_err, "no engine configuration fits (cluster_size %d)", opt->cluster_size);
     return AMMMSE_ERR_UNSUPPORTED;
   }
@@ -310,6 +341,16 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.vold_glob = plan.cluster ? plan.vglob : 0;
   a.sb_bytes = plan.sb;
   a.scratch = reinterpret_cast<unsigned char*>(workspace) + 256;
+  a.tcm = plan.cluster ? plan.tc : 0;
+  if (a.tcm) {  // H planes after the V_old slots, 256-byte aligned
+    int sms2 = 0;
+    cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
+    const size_t rsz = dims->dtype == AMMMSE_COMPLEX64 ? 4 : 8;
+    const size_t ncol = (size_t)(dims->K / plan.cluster) * dims->d;
+    size_t off = plan.vglob ? (size_t)sms2 * 2 * (size_t)dims->M * ncol * rsz : 0;
+    off = (off + 255) & ~(size_t)255;
+    a.hplanes = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(workspace) + 256 + off);
+  }
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
   // debug: per-phase clock totals (AMMMSE_PROFILE_PHASES=1), printed to stderr
   static unsigned long long* prof_buf = nullptr;

@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "ammmse_engine.cuh"
+#include "tc_gemm.cuh"
 
 namespace ammmse {
 
@@ -314,6 +315,15 @@ __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>*
 }
 
 constexpr int kStreamStages = 4;
+constexpr int kTcStages = 3;  // cp.async ring depth of the tensor-core GEMM
+constexpr int kTcCols = 256;  // TMEM columns allocated per CTA (tensor-core mode)
+
+// tensor-core mode shape rules (UMMA M = 64/128 tiles, N % 16, K steps of 8)
+__host__ __device__ inline bool tc_shape_ok(int M, int KN, int ncol) {
+  if (M % 128 || !(KN == 64 || KN % 128 == 0) || ncol % 16 || ncol > 256) return false;
+  const int tA = M / 128, tB = KN >= 128 ? KN / 128 : 1;
+  return 2 * ncol * (tA > tB ? tA : tB) <= kTcCols;
+}
 
 constexpr int kStreamRY = 4, kStreamRX = 2, kStreamTPT = 4;
 
@@ -327,15 +337,18 @@ struct CLayout {
   int M, K, C, KL, KN, KD, ncol, ldh, ldv, ldg;
   int hres;  // 1: H resident in SMEM;  0: H streamed from global through `stage`
   int vglob; // 1: the second V buffer lives in a per-CTA global scratch slot (L2)
+  int tc;    // 1: tensor-core GEMMs; the H region holds the tcgen05 operand ring
+  int tc_a, tc_b;  // floats of one ring stage's A / B tile
   int SB;    // staging buffer size (complex elements) when streamed
   size_t nH, nV, nG;
   size_t oH, oV0, oV1, oG0, oG1, oUall, oPall, oDown;  // R offsets (planar / RC)
   size_t dbl_off, bytes;
 
   __host__ __device__ void init(int M_, int K_, int C_, int hres_ = 1, int vglob_ = 0,
-                                int sb_bytes = 20480) {
+                                int sb_bytes = 20480, int tc_ = 0) {
     hres = hres_;
     vglob = vglob_;
+    tc = tc_;
     SB = sb_bytes / (int)(2 * sizeof(R));  // per staging buffer (kStreamStages of them)
     M = M_;
     K = K_;
@@ -352,6 +365,9 @@ struct CLayout {
     // resident: planar H (2 planes of KN x ldh); streamed: kStreamStages buffers of SB
     // interleaved complex = 2*kStreamStages*SB reals = 2 "planes" of kStreamStages*SB
     nH = hres ? (size_t)KN * ldh : (size_t)kStreamStages * SB;
+    tc_a = 4 * (KN > M ? KN : M) * tcg::KC;
+    tc_b = 4 * ncol * tcg::KC;
+    if (tc) nH = ((size_t)kTcStages * (tc_a + tc_b) + 1) / 2;  // ring floats = 2 nH
     oH = 0;
     oV0 = oH + 2 * nH;
     oV1 = oV0 + 2 * nV;
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   const int tid = threadIdx.x;
 
   CLayout<R, NN, DD> L;
-  L.init(a.M, a.K, C, a.hres, a.vold_glob, a.sb_bytes);
+  L.init(a.M, a.K, C, a.hres, a.vold_glob, a.sb_bytes, a.tcm);
   const bool hres = a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
@@ -424,6 +440,38 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   double* ust = dp; dp += KL;
   double* xs = dp; dp += XS_COUNT;
   double* red = dp;
+
+  // ---- tensor-core mode: TMEM accumulator, per-stage mbarriers ----
+  __shared__ uint64_t tc_mbar[kTcStages];
+  __shared__ uint32_t tc_uses[kTcStages];
+  __shared__ uint32_t tc_tmem_slot;
+  tcg::Ring ring;
+  ring.stage = reinterpret_cast<float*>(base + L.oH);
+  ring.a_floats = L.tc_a;
+  ring.b_floats = L.tc_b;
+  ring.mbar = tc_mbar;
+  ring.uses = tc_uses;
+  ring.tmem = 0;
+  const float* hpB = nullptr;  // pre-split H planes (rows r, K = m), this cluster's slot
+  const float* hpA = nullptr;  // pre-split H^T planes (rows m, K = r)
+  if (L.tc) {
+    if (tid == 0) {
+      for (int q = 0; q < kTcStages; ++q) {
+        umma::mbar_init(&tc_mbar[q], 1);
+        tc_uses[q] = 0;
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if ((tid >> 5) == 0) umma::tmem_alloc<kTcCols>(&tc_tmem_slot);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    ring.tmem = tc_tmem_slot;
+    const size_t hp = (size_t)8 * L.KN * L.M;
+    float* slot = a.hplanes + (size_t)(blockIdx.x / C) * hp;
+    hpB = slot;
+    hpA = slot + (size_t)4 * L.KN * L.M;
+  }
 
   // fixed-order cluster sum / first-nonzero of an exchange slot
   auto xsum = [&](int slot) {
@@ -592,7 +640,25 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
                                 xi[o] = x_i;
                                 pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
                               };
-    if (hres)
+    if constexpr (sizeof(R) == 4) {
+      if (L.tc) {  // ∇' = H^H Ŷ on tcgen05 (signs +,-), epilogue per (row, col, part)
+        tcg::gemm<kTcStages>(ring, M, ncol, KN, hpA, (const float*)Gr[ysrc],
+                             (const float*)Gi[ysrc], ldg, 1.f, -1.f);
+        tcg::for_each_d(ring, M, ncol, [&](int p, int q, int part, float g) {
+          const int o = p * ldv + q;
+          const R* vc = part ? vci : vcr;
+          R* x = part ? xi : xr;
+          R v = vc[o];
+          if (extrap) v = v + om * (v - x[o]);
+          const R xv = v - st * g;
+          x[o] = xv;
+          pw += (double)xv * (double)xv;
+        });
+        umma::fence_before();
+      }
+    }
+    if (L.tc) {
+    } else if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
     else if ((M / 4) * (ncol / 4) < (int)blockDim.x &&
              stream2_ok<R, 2, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
@@ -619,7 +685,18 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       gr[p * ldg + q] = cr;
       gi[p * ldg + q] = ci;
     };
-    if (hres)
+    if constexpr (sizeof(R) == 4) {
+      if (L.tc) {  // G = H V on tcgen05 (signs -,+)
+        tcg::gemm<kTcStages>(ring, KN, ncol, M, hpB, (const float*)Vr[src], (const float*)Vi[src],
+                             ldv, -1.f, 1.f);
+        tcg::for_each_d(ring, KN, ncol, [&](int p, int q, int part, float g) {
+          (part ? gi : gr)[p * ldg + q] = g;
+        });
+        umma::fence_before();
+      }
+    }
+    if (L.tc) {
+    } else if (hres)
       cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
     else if (stream2_ok<R, 2, 4, false>(KN, ncol, M, ldv, L.SB, blockDim.x))
       cgemm_stream2<R, 2, 4, kStreamStages, false>(KN, ncol, M, Hcur, M, stage, L.SB, Vr[src],
@@ -646,6 +723,15 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     {
       const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
       Hcur = Hg;
+      if constexpr (sizeof(R) == 4) {
+        if (L.tc) {  // this CTA's share of the pre-split H / H^T planes (rows r0..r1)
+          const int r0 = crank * (KN / C), r1 = (crank + 1) * (KN / C);
+          const float2* H2 = reinterpret_cast<const float2*>(Hg);
+          tcg::split_planes(H2, KN, M, false, const_cast<float*>(hpB), r0, r1);
+          tcg::split_planes(H2, KN, M, true, const_cast<float*>(hpA), r0, r1);
+          __threadfence();  // visible to the other CTAs' cp.async before the next cluster barrier
+        }
+      }
       if (hres) {
         for (int i = tid; i < KN * M; i += blockDim.x) {
           const int row = i / M, col = i - row * M;
@@ -972,6 +1058,10 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     pc.mark(9);
   }
   pc.flush();
+  if (L.tc) {
+    __syncthreads();
+    if ((tid >> 5) == 0) umma::tmem_dealloc<kTcCols>(ring.tmem);
+  }
 }
 
 }  // namespace ammmse

@@ -81,6 +81,8 @@ struct EngineArgs {
   int vold_glob;  // cluster engine: second V buffer in global scratch (1)
   int sb_bytes;   // cluster engine: bytes per cp.async staging buffer
   unsigned char* scratch;  // cluster engine: per-CTA global scratch (vold_glob)
+  int tcm;                 // cluster engine: tcgen05 3xTF32 GEMMs (streamed H planes)
+  float* hplanes;          // tcm: per-cluster pre-split H planes (8 x KN x M floats each)
   unsigned long long* prof;  // debug: per-phase clock64 totals (nullptr = off)
   long long B;
   unsigned long long* counter;

@@ -9,7 +9,7 @@ struct KernelEntry {
   const void* bounds;                          // ammmse_bounds_kernel<R, N>
   size_t (*smem_bytes)(int M, int K);          // Layout<R, N, d>::bytes
   const void* cluster_solve;                   // ammmse_cluster_kernel<R, N, d> (1 cluster / realization)
-  size_t (*cluster_smem_bytes)(int M, int K, int C, int hres, int vglob, int sb);  // CLayout::bytes
+  size_t (*cluster_smem_bytes)(int M, int K, int C, int hres, int vglob, int sb, int tc);  // CLayout::bytes
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4

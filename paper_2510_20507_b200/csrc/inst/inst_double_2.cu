@@ -5,9 +5,9 @@
 namespace ammmse {
 namespace {
 template <int DD>
-size_t cluster_smem_fn(int M, int K, int C, int hres, int vglob, int sb) {
+size_t cluster_smem_fn(int M, int K, int C, int hres, int vglob, int sb, int tc) {
   CLayout<double, 2, DD> L;
-  L.init(M, K, C, hres, vglob, sb);
+  L.init(M, K, C, hres, vglob, sb, tc);
   return L.bytes;
 }
 template <int DD>

@@ -277,7 +277,7 @@ class AmmmseEngine:
     def solve(self, channels, noise_power, p_max, weights, init_precoders, *, gamma, omega,
               eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
               out: BatchResult | None = None, stream=None, cluster_size: int = 0,
-              h_placement: int = 0) -> BatchResult:
+              h_placement: int = 0, tensor_cores: int = 0) -> BatchResult:
         torch = _torch()
         dims = self.dims(channels, init_precoders)
         self.check(dims)
@@ -315,7 +315,8 @@ class AmmmseEngine:
             gamma=0.0 if (safe or g_arr is not None) else float(gamma), gamma_safe=1 if safe else 0,
             max_iters=int(max_iters), omega=0.0 if o_arr is not None else float(omega),
             eps1=float(eps1), eps2=float(eps2), latch_stage=1 if latch_stage else 0,
-            cluster_size=int(cluster_size), h_placement=int(h_placement), reserved=0)
+            cluster_size=int(cluster_size), h_placement=int(h_placement),
+            tensor_cores=int(tensor_cores))
         prob = _native.AmmmseProblem(channels.data_ptr(), noise_power.data_ptr(), p_max.data_ptr(),
                                      weights.data_ptr(), init_precoders.data_ptr(),
                                      None if g_arr is None else g_arr.data_ptr(),
@@ -328,7 +329,7 @@ class AmmmseEngine:
         ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
         if ws_bytes == 0:
             raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
-                              f"h_placement={h_placement})")
+                              f"h_placement={h_placement}, tensor_cores={tensor_cores})")
         ws = self._workspace(ws_bytes)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
@@ -391,7 +392,7 @@ def _validate_host_inputs(H, sigma2, p_max, weights, V0):
 def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, options: SolverOptions,
                      snr_db: float = 10.0, record_trace: bool = False, device=None,
                      step_gamma=None, step_omega=None, cluster_size: int = 0,
-                     h_placement: int = 0) -> BatchResult:
+                     h_placement: int = 0, tensor_cores: int = 0) -> BatchResult:
     """Solve B realizations from host arrays; returns a host BatchResult.
 
     channels (B, K, N, M), init_precoders (B, K, M, d): complex64 or
@@ -436,7 +437,7 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
                     torch.from_numpy(V0).to(dev), gamma=gamma, omega=omega, eps1=options.eps1,
                     eps2=options.eps2, max_iters=options.max_iters, latch_stage=options.latch_stage,
                     record_trace=record_trace, cluster_size=cluster_size,
-                    h_placement=h_placement)
+                    h_placement=h_placement, tensor_cores=tensor_cores)
     return out.to_host()
 
 

@@ -214,3 +214,23 @@ def test_cluster_streamed_odd_stage_rows_complex64(cuda):
         r = oracle_solve(b, **kw)
         rel = np.abs(g.wsr_bits - r["wsr_bits"]) / np.abs(r["wsr_bits"])
         assert rel.max() <= WSR_RTOL_C64, (hp, rel)
+
+
+@pytest.mark.parametrize("M,K,N,d,csize", [(128, 8, 4, 4, 2), (256, 16, 2, 2, 4), (128, 32, 2, 2, 1)])
+def test_cluster_tensor_core_gemms_complex64(cuda, M, K, N, d, csize):
+    """tcgen05 3xTF32 GEMMs (tensor_cores=1) against the fp64 oracle and the FFMA
+    path on the same inputs (M >= 128 shapes the tensor-core mode accepts)."""
+    b = build_batch(M, N, K, d, 3, p_max=50.0, weights="uniform", dtype=np.complex64, seed0=21)
+    kw = dict(gamma=0.002, omega=0.8, eps2=1e-5, max_iters=120)
+    opts = SolverOptions(algorithm="ammmse", **kw)
+    tc = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                          record_trace=True, cluster_size=csize, tensor_cores=1)
+    ff = run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders, opts,
+                          record_trace=True, cluster_size=csize, tensor_cores=2)
+    r = oracle_solve(b, **kw)
+    for g in (tc, ff):
+        rel = np.abs(g.wsr_bits - r["wsr_bits"]) / np.abs(r["wsr_bits"])
+        assert rel.max() <= WSR_RTOL_C64, rel
+    # per-iteration WSR trajectories of the two GEMM engines agree closely
+    n = min(tc.iterations.min(), ff.iterations.min())
+    np.testing.assert_allclose(tc.trace[:, :n, 1], ff.trace[:, :n, 1], rtol=1e-5)
