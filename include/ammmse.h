@@ -116,8 +116,9 @@ typedef struct AmmmseOptions {
   int32_t h_placement; /* cluster engine only: 0 auto, 1 H resident in every CTA's SMEM,
                           2 H streamed from HBM/L2 through a cp.async ring, 3 streamed H and
                           the previous precoders in a per-CTA global scratch slot */
-  int32_t tensor_cores;/* cluster engine, complex64: 0 auto (tcgen05 3xTF32 GEMMs where the shape
-                          and shared memory allow), 1 require them, 2 FP32 FFMA GEMMs only */
+  int32_t tensor_cores;/* cluster engine, complex64: 1 tcgen05 3xTF32 GEMMs (streamed H planes,
+                          TMEM accumulators) where shape and shared memory allow; 0 / 2 FP32
+                          FFMA GEMMs (0 = automatic = FFMA: measured faster in round 1) */
 } AmmmseOptions;
 
 /* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */

@@ -107,9 +107,12 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_core
         continue;
       // streamed H moves 16-byte pieces: complex64 rows need an even length
       if (!hres && d->dtype == AMMMSE_COMPLEX64 && (d->M % 2)) continue;
-      // tensor-core GEMMs (streamed pre-split H planes) when the shape allows
+      // tensor-core GEMMs (streamed pre-split H planes): opt-in (tensor_cores = 1).
+      // Measured round 1: the one-K-step-per-stage ring is latency bound and
+      // slower than the FFMA path (large 407 vs 582 realizations/s), so the
+      // automatic plan keeps FFMA.
       const int ncol = (d->K / c) * d->d;
-      if (!hres && d->dtype == AMMMSE_COMPLEX64 && tensor_cores != 2 &&
+      if (!hres && d->dtype == AMMMSE_COMPLEX64 && tensor_cores == 1 &&
           ammmse::tc_shape_ok(d->M, d->K * d->N, ncol)) {
         const size_t st = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb, 1);
         if (st <= (size_t)lim) {
