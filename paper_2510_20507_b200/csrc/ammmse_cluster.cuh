@@ -620,37 +620,51 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       }
     }
   };
-  // GEMM-A + extrapolation + step, returns cluster-wide ‖X‖²
-  auto grad_step = [&](int ysrc, int vcur, int dst, double step, double omega, bool extrap) {
-    const R* vcr = Vr[vcur];
-    const R* vci = Vi[vcur];
-    R* xr = Vr[dst];
-    R* xi = Vi[dst];
+  // GEMM-A + extrapolation + step, returns cluster-wide ‖X‖².
+  //   V̂ = V[vc] + ω (V[vc] − V[vo]);  X = V̂ − step ∇ -> V[vx];  save: V[vo] <- old V[vc]
+  // With V_old in global scratch (L.vglob) the current precoders stay pinned in
+  // the SMEM slot 0 (vc = vx = 0, vo = 1, save): GEMM-B always reads SMEM.
+  auto grad_step = [&](int ysrc, int vc, int vo, int vx, bool save, double step, double omega,
+                       bool extrap) {
+    const R* vcr = Vr[vc];
+    const R* vci = Vi[vc];
+    R* vor = Vr[vo];
+    R* voi = Vi[vo];
+    R* xr = Vr[vx];
+    R* xi = Vi[vx];
     const R st = (R)step, om = (R)omega;
     double pw = 0.0;
     auto epi = [&](int p, int q, R gr, R gi) {
-                                const int o = p * ldv + q;
-                                R vr = vcr[o], vi = vci[o];
-                                if (extrap) {
-                                  vr = vr + om * (vr - xr[o]);
-                                  vi = vi + om * (vi - xi[o]);
-                                }
-                                const R x_r = vr - st * gr, x_i = vi - st * gi;
-                                xr[o] = x_r;
-                                xi[o] = x_i;
-                                pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
-                              };
+      const int o = p * ldv + q;
+      const R cr0 = vcr[o], ci0 = vci[o];
+      R vr = cr0, vi = ci0;
+      if (extrap) {
+        vr = vr + om * (vr - vor[o]);
+        vi = vi + om * (vi - voi[o]);
+      }
+      const R x_r = vr - st * gr, x_i = vi - st * gi;
+      if (save) {
+        vor[o] = cr0;
+        voi[o] = ci0;
+      }
+      xr[o] = x_r;
+      xi[o] = x_i;
+      pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
+    };
     if constexpr (sizeof(R) == 4) {
       if (L.tc) {  // ∇' = H^H Ŷ on tcgen05 (signs +,-), epilogue per (row, col, part)
         tcg::gemm<kTcStages>(ring, M, ncol, KN, hpA, (const float*)Gr[ysrc],
                              (const float*)Gi[ysrc], ldg, 1.f, -1.f);
         tcg::for_each_d(ring, M, ncol, [&](int p, int q, int part, float g) {
           const int o = p * ldv + q;
-          const R* vc = part ? vci : vcr;
+          const R* vcp = part ? vci : vcr;
+          R* vop = part ? voi : vor;
           R* x = part ? xi : xr;
-          R v = vc[o];
-          if (extrap) v = v + om * (v - x[o]);
+          const R c0 = vcp[o];
+          R v = c0;
+          if (extrap) v = v + om * (v - vop[o]);
           const R xv = v - st * g;
+          if (save) vop[o] = c0;
           x[o] = xv;
           pw += (double)xv * (double)xv;
         });
@@ -884,19 +898,22 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       build_yhat(oth);
       __syncthreads();
       pc.mark(3);
-      const double power = grad_step(oth, cur, oth, ctl.step, ctl.omega, extrap);
+      const bool pin = L.vglob;  // current precoders pinned in SMEM slot 0
+      const int vx = pin ? 0 : oth;
+      const double power = pin ? grad_step(oth, 0, 1, 0, true, ctl.step, ctl.omega, extrap)
+                               : grad_step(oth, cur, oth, oth, false, ctl.step, ctl.omega, extrap);
       double scale = 1.0;
       if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
       if (scale != 1.0) {
         const R sc = (R)scale;
         for (int i = tid; i < M * ncol; i += blockDim.x) {
-          Vr[oth][i] *= sc;
-          Vi[oth][i] *= sc;
+          Vr[vx][i] *= sc;
+          Vi[vx][i] *= sc;
         }
       }
       __syncthreads();
       pc.mark(4);
-      gemm_hv(oth, oth);
+      gemm_hv(vx, oth);
       __syncthreads();
       pc.mark(5);
       gram_partials(Gr[oth], Gi[oth], 1);
@@ -1009,14 +1026,15 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       if (st == 0) {
         build_yhat(oth);
         __syncthreads();
-        const double power = grad_step(oth, cur, oth, 2.0 * ctl.gamma_safe, 0.0, false);
+        const int rc = L.vglob ? 0 : cur, rx = L.vglob ? 1 : oth;
+        const double power = grad_step(oth, rc, rx, rx, false, 2.0 * ctl.gamma_safe, 0.0, false);
         double scale = 1.0;
         if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
         double dsum = 0.0, vsum = 0.0;
         for (int i = tid; i < M * ncol; i += blockDim.x) {
-          const double a_r = (double)Vr[cur][i], a_i = (double)Vi[cur][i];
-          const double dr = a_r - (double)((R)(Vr[oth][i] * (R)scale));
-          const double di = a_i - (double)((R)(Vi[oth][i] * (R)scale));
+          const double a_r = (double)Vr[rc][i], a_i = (double)Vi[rc][i];
+          const double dr = a_r - (double)((R)(Vr[rx][i] * (R)scale));
+          const double di = a_i - (double)((R)(Vi[rx][i] * (R)scale));
           dsum += dr * dr + di * di;
           vsum += a_r * a_r + a_i * a_i;
         }
@@ -1040,7 +1058,8 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         RC<R>* Vg = reinterpret_cast<RC<R>*>(a.Vout) + ((size_t)r * K + k0) * M * DD;
         for (int i = tid; i < KL * M * DD; i += blockDim.x) {
           const int kl = i / (M * DD), rem = i - kl * M * DD, m = rem / DD, s = rem - m * DD;
-          Vg[i] = RC<R>{Vr[cur][m * ldv + kl * DD + s], Vi[cur][m * ldv + kl * DD + s]};
+          const int vcur = L.vglob ? 0 : cur;
+          Vg[i] = RC<R>{Vr[vcur][m * ldv + kl * DD + s], Vi[vcur][m * ldv + kl * DD + s]};
         }
       }
       if (tid == 0 && crank == 0) {
