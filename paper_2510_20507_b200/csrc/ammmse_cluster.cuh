@@ -201,6 +201,11 @@ __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>*
   const int KC = stream2_kc<R>(CONJT, P, SB);
   const int lds = CONJT ? P : KC + EPC;
   const int nchunks = (KD + KC - 1) / KC;
+  if constexpr (RY <= 4) {  // operands in shared memory -> LDS (measured slower for 8-row tiles)
+    __builtin_assume(__isShared(stage));
+    __builtin_assume(__isShared(Br));
+    __builtin_assume(__isShared(Bi));
+  }
   const int QT = Q / RX, ntiles = (P / RY) * QT;
   const bool active = threadIdx.x < ntiles;
   const int tile = active ? threadIdx.x : 0;

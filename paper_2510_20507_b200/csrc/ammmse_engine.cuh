@@ -321,6 +321,11 @@ __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R*
                                            const R* __restrict__ Ai, int lda,
                                            const R* __restrict__ Br, const R* __restrict__ Bi,
                                            int ldb, Epi epi) {
+  // operands live in shared memory: let the compiler emit LDS (not generic LD)
+  __builtin_assume(__isShared(Ar));
+  __builtin_assume(__isShared(Ai));
+  __builtin_assume(__isShared(Br));
+  __builtin_assume(__isShared(Bi));
   const int QT = Q / RX, tiles = (P / RY) * QT;
   const int w = threadIdx.x;
   const bool active = w < tiles * S;
