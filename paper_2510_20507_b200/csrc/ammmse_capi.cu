@@ -258,7 +258,12 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     snprintf(g_err, sizeof g_err, "workspace missing or too small");
     return AMMMSE_ERR_WORKSPACE;
   }
-  const void* func = plan.cluster ? plan.e->cluster_solve : plan.e->solve;
+  const void* func = plan.cluster ? (plan.tc ? plan.e->cluster_solve_tc : plan.e->cluster_solve)
+                                  : plan.e->solve;
+  if (!func) {
+    snprintf(g_err, sizeof g_err, "no kernel instantiation for this plan");
+    return AMMMSE_ERR_UNSUPPORTED;
+  }
   const size_t smem = plan.smem;
   const int threads = plan.threads;
   cudaStream_t s = (cudaStream_t)stream;

@@ -394,7 +394,9 @@ struct CLayout {
   }
 };
 
-template <typename R, int NN, int DD>
+// TC = true: the tcgen05 GEMM variant (separate instantiation, so the FFMA
+// kernel carries none of its code, registers or local arrays).
+template <typename R, int NN, int DD, bool TC = false>
 __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   ring.tmem = 0;
   const float* hpB = nullptr;  // pre-split H planes (rows r, K = m), this cluster's slot
   const float* hpA = nullptr;  // pre-split H^T planes (rows m, K = r)
-  if (L.tc) {
+  if (TC && L.tc) {
     if (tid == 0) {
       for (int q = 0; q < kTcStages; ++q) {
         umma::mbar_init(&tc_mbar[q], 1);
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
     };
     if constexpr (sizeof(R) == 4) {
-      if (L.tc) {  // ∇' = H^H Ŷ on tcgen05 (signs +,-), epilogue per (row, col, part)
+      if (TC && L.tc) {  // ∇' = H^H Ŷ on tcgen05 (signs +,-), epilogue per (row, col, part)
         tcg::gemm<kTcStages>(ring, M, ncol, KN, hpA, (const float*)Gr[ysrc],
                              (const float*)Gi[ysrc], ldg, 1.f, -1.f);
         tcg::for_each_d(ring, M, ncol, [&](int p, int q, int part, float g) {
@@ -676,7 +678,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         umma::fence_before();
       }
     }
-    if (L.tc) {
+    if (TC && L.tc) {
     } else if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
     else if ((M / 4) * (ncol / 4) < (int)blockDim.x &&
@@ -705,7 +707,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       gi[p * ldg + q] = ci;
     };
     if constexpr (sizeof(R) == 4) {
-      if (L.tc) {  // G = H V on tcgen05 (signs -,+)
+      if (TC && L.tc) {  // G = H V on tcgen05 (signs -,+)
         tcg::gemm<kTcStages>(ring, KN, ncol, M, hpB, (const float*)Vr[src], (const float*)Vi[src],
                              ldv, -1.f, 1.f);
         tcg::for_each_d(ring, KN, ncol, [&](int p, int q, int part, float g) {
@@ -714,7 +716,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         umma::fence_before();
       }
     }
-    if (L.tc) {
+    if (TC && L.tc) {
     } else if (hres)
       cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
     else if (stream2_ok<R, 2, 4, false>(KN, ncol, M, ldv, L.SB, blockDim.x))
@@ -743,7 +745,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
       Hcur = Hg;
       if constexpr (sizeof(R) == 4) {
-        if (L.tc) {  // this CTA's share of the pre-split H / H^T planes (rows r0..r1)
+        if (TC && L.tc) {  // this CTA's share of the pre-split H / H^T planes (rows r0..r1)
           const int r0 = crank * (KN / C), r1 = (crank + 1) * (KN / C);
           const float2* H2 = reinterpret_cast<const float2*>(Hg);
           tcg::split_planes(H2, KN, M, false, const_cast<float*>(hpB), r0, r1);
@@ -1082,7 +1084,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     pc.mark(9);
   }
   pc.flush();
-  if (L.tc) {
+  if (TC && L.tc) {
     __syncthreads();
     if ((tid >> 5) == 0) umma::tmem_dealloc<kTcCols>(ring.tmem);
   }

@@ -123,17 +123,17 @@ struct Layout {
     dbl_off = ((nR * sizeof(R)) + 15) & ~(size_t)15;
     bytes = dbl_off + dbl_bytes();
   }
-  // fp64 region, in doubles:
-  //   gram   K*NN*NN cd   (2 doubles each)
-  //   ucache K*NN*DD cd
-  //   wcache K*DD*DD cd
-  //   lndetw K
-  //   alpha  K
-  //   fu fw fv rate  4K
+  // fp64 region, in doubles (banks [2]: the pipelined loop runs WSR(t) and
+  // K1(t+1) concurrently, so per-iteration user state is double-buffered):
+  //   gram[2]   K*NN*NN cd each (2 doubles per cd): [0] Ĝ for K1, [1] G_new for WSR
+  //   ucache[2] K*NN*DD cd, wcache[2] K*DD*DD cd   (bank = iteration parity)
+  //   lndetw[2], fu[2], fw[2]  K each
+  //   alpha, fv, rate  K each
   //   ustat, ust2  K each (k1 / wsr per-user status, stored as double)
   //   red    32
   __host__ __device__ size_t dbl_count() const {
-    return (size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + K + K + 4 * K + 2 * K + 32;
+    return (size_t)2 * (2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + 3 * K) + 3 * K +
+           2 * K + 32;
   }
   __host__ __device__ size_t dbl_bytes() const { return dbl_count() * sizeof(double); }
 };
@@ -178,6 +178,7 @@ struct Ctl {
   double f_u, f_w, f_v, wsr;
   double scale, total_power;
   double vscale[2];  // V[i] holds X_i unscaled; the precoders are vscale[i] * X_i
+  int wn_next;       // stage flag of the next iteration (decided by the state machine)
 };
 
 // ---------------------------------------------------------------------------
@@ -466,8 +467,9 @@ struct Engine {
   // smem views
   R *Hr, *Hi, *Vr[2], *Vi[2], *Gr[2], *Gi[2];
   RC<R>*Uf, *Pf, *Df;  // per user N x d, R
-  cd *gram, *ucache, *wcache;
-  double *lndetw, *alpha, *fu, *fw, *fv, *rate, *ustat, *ust2, *red;
+  cd *gramb[2], *ucb[2], *wcb[2];
+  double *lndb[2], *fub[2], *fwb[2];
+  double *alpha, *fv, *rate, *ustat, *ust2, *red;
   L_t L;
 
   __device__ void bind(unsigned char* smem, int M, int K) {
@@ -483,13 +485,15 @@ struct Engine {
     Pf = Uf + K * NN * DD;
     Df = Pf + K * NN * DD;
     double* d = reinterpret_cast<double*>(smem + L.dbl_off);
-    gram = reinterpret_cast<cd*>(d); d += 2 * K * NN * NN;
-    ucache = reinterpret_cast<cd*>(d); d += 2 * K * NN * DD;
-    wcache = reinterpret_cast<cd*>(d); d += 2 * K * DD * DD;
-    lndetw = d; d += K;
+    for (int b = 0; b < 2; ++b) {
+      gramb[b] = reinterpret_cast<cd*>(d); d += 2 * K * NN * NN;
+      ucb[b] = reinterpret_cast<cd*>(d); d += 2 * K * NN * DD;
+      wcb[b] = reinterpret_cast<cd*>(d); d += 2 * K * DD * DD;
+      lndb[b] = d; d += K;
+      fub[b] = d; d += K;
+      fwb[b] = d; d += K;
+    }
     alpha = d; d += K;
-    fu = d; d += K;
-    fw = d; d += K;
     fv = d; d += K;
     rate = d; d += K;
     ustat = d; d += K;
@@ -498,10 +502,15 @@ struct Engine {
   }
 
   // Receiver / weight / gradient-factor update of user k from the Gram in
-  // `gram` and the work G (Ĝ).  Writes U/P/D (R) for the Ŷ phase, the fp64
-  // U/W caches and the per-user objective terms / status.
+  // gramb[0] and the work G (Ĝ).  Reads W_prev from bank `bin`; writes U/P/D
+  // (R) for the Ŷ phase, the fp64 U/W caches and objective terms of bank
+  // `bout`, and the per-user status.
   __device__ void k1_user(int k, const R* Gwr, const R* Gwi, int ldg, double sigma2, bool weighted,
-                          bool want_f) {
+                          bool want_f, int bin, int bout) {
+    const cd* gram = gramb[0];
+    const cd* wprev = wcb[bin];
+    cd* ucache = ucb[bout];
+    cd* wcache = wcb[bout];
     cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -517,9 +526,9 @@ struct Engine {
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
-      for (int q = 0; q < DD; ++q) Wp[p][q] = wcache[(k * DD + p) * DD + q];
+      for (int q = 0; q < DD; ++q) Wp[p][q] = wprev[(k * DD + p) * DD + q];
     K1Out<NN, DD> o;
-    k1_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], Wp, lndetw[k], weighted, want_f, o);
+    k1_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], Wp, lndb[bin][k], weighted, want_f, o);
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
@@ -534,14 +543,18 @@ struct Engine {
     for (int p = 0; p < DD; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q) wcache[(k * DD + p) * DD + q] = o.W[p][q];
-    lndetw[k] = o.lndetw;
-    fu[k] = o.fu;
-    fw[k] = o.fw;
+    lndb[bout][k] = o.lndetw;
+    fub[bout][k] = o.fu;
+    fwb[bout][k] = o.fw;
     ustat[k] = o.status;
   }
 
   // Rate and f_after_v terms of user k from the Gram of G_new.
-  __device__ void wsr_user(int k, const R* Gnr, const R* Gni, int ldg, double sigma2) {
+  // Gram of G_new in gramb[1]; U / W of bank b.
+  __device__ void wsr_user(int k, const R* Gnr, const R* Gni, int ldg, double sigma2, int b) {
+    const cd* gram = gramb[1];
+    const cd* ucache = ucb[b];
+    const cd* wcache = wcb[b];
     cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -561,7 +574,7 @@ struct Engine {
       for (int q = 0; q < DD; ++q) W[p][q] = wcache[(k * DD + p) * DD + q];
     double r, f;
     int st;
-    wsr_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], U, W, lndetw[k], r, f, st);
+    wsr_math<NN, DD>(Tg, Gkk, sigma2, alpha[k], U, W, lndb[b][k], r, f, st);
     rate[k] = r;
     fv[k] = f;
     ust2[k] = st;
@@ -570,7 +583,7 @@ struct Engine {
   // Gram of user k over `ncols` columns of X, computed by one warp (lanes over
   // columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
   __device__ void gram_user(int k, const R* __restrict__ Xr, const R* __restrict__ Xi, int ld,
-                            int ncols, int lane) {
+                            int ncols, int lane, cd* gram) {
     double sr[NN][NN], si[NN][NN];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -665,12 +678,14 @@ struct Engine {
   // Gram(Ĝ) on all warps | receiver / weight / gradient factors with lanes =
   // users (as few warps as possible: the fp64 per-user code is issued once per
   // warp) | Ŷ on all threads.  Two block barriers.
-  __device__ void phase_k1_yhat(R* Gwr, R* Gwi, double sigma2, bool weighted, bool want_f) {
+  __device__ void phase_k1_yhat(R* Gwr, R* Gwi, double sigma2, bool weighted, bool want_f,
+                                int bin, int bout) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int K = L.K, KD = L.KD, ldg = L.ldg;
-    for (int k = warp; k < K; k += nw) gram_user(k, Gwr, Gwi, ldg, KD, lane);
+    for (int k = warp; k < K; k += nw) gram_user(k, Gwr, Gwi, ldg, KD, lane, gramb[0]);
     __syncthreads();
-    for (int k = threadIdx.x; k < K; k += blockDim.x) k1_user(k, Gwr, Gwi, ldg, sigma2, weighted, want_f);
+    for (int k = threadIdx.x; k < K; k += blockDim.x)
+      k1_user(k, Gwr, Gwi, ldg, sigma2, weighted, want_f, bin, bout);
     __syncthreads();
     build_yhat(Gwr, Gwi, ldg, K, KD);
   }
@@ -831,9 +846,9 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       }
       for (int k = tid; k < K; k += blockDim.x) {
         e.alpha[k] = a.alpha[(size_t)r * K + k];
-        e.lndetw[k] = 0.0;  // W_prev = I at t = 1 (solvers.py:429-430)
+        e.lndb[0][k] = 0.0;  // W_prev = I at t = 1 (solvers.py:429-430); K1(1) reads bank 0
         for (int p = 0; p < DD; ++p)
-          for (int q = 0; q < DD; ++q) e.wcache[(k * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
+          for (int q = 0; q < DD; ++q) e.wcb[0][(k * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
       }
       if (tid == 0) {
         ctl.sigma2 = a.sigma2[r];
@@ -859,12 +874,12 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
     __syncthreads();
 
     // ---------------- bounds: kappa, gamma_safe (objective.py:216-240) ----------------
-    user_grams<R, NN>(e.Hr, e.Hi, ldh, M, K, e.gram);
+    user_grams<R, NN>(e.Hr, e.Hi, ldh, M, K, e.gramb[0]);
     __syncthreads();
     for (int k = tid; k < K; k += blockDim.x) {
       cd G[NN][NN];
       for (int p = 0; p < NN; ++p)
-        for (int q = 0; q < NN; ++q) G[p][q] = e.gram[(k * NN + p) * NN + q];
+        for (int q = 0; q < NN; ++q) G[p][q] = e.gramb[0][(k * NN + p) * NN + q];
       e.rate[k] = herm_eig_max<NN>(G);
     }
     __syncthreads();
@@ -884,28 +899,61 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
     e.gemm_hv(0, 0, 1, 0.0);
     __syncthreads();
 
-    // ---------------- main loop (solvers.py:440-505) ----------------
-    // Per iteration: [warp-fused Gram(Ĝ) -> U/W/Ŷ] | GEMM-A + projection |
-    // GEMM-B (+ next Ĝ) | [warp-fused Gram(G) -> rates] | warp-0 reductions and
-    // state machine: 7 block barriers (+2 inside the power reduction).
+    // ---------------- K1(1) (solvers.py:440-460 at t = 1) ----------------
+    // Stage flag of iteration t (solvers.py:449-459), from the shared state.
+    auto stage_flag = [&]() -> bool {
+      if (ctl.latched) return true;
+      double rs = INFINITY;
+      if (ctl.nhist >= 2) {
+        const double den = fabs(ctl.wsr_prev);
+        rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
+      }
+      return rs <= a.eps1;
+    };
+    bool wn = stage_flag();  // the flag K1(t) was computed with
+    {
+      const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+      for (int k = warp; k < K; k += nw) e.gram_user(k, e.Gr[1], e.Gi[1], ldg, KD, lane, e.gramb[0]);
+      __syncthreads();
+      for (int k = tid; k < K; k += blockDim.x)
+        e.k1_user(k, e.Gr[1], e.Gi[1], ldg, ctl.sigma2, wn, true, 0, 1);
+      __syncthreads();
+    }
+
+    // ---------------- main loop (solvers.py:440-505), software-pipelined ----------------
+    // Per iteration t: Ŷ(t) | GEMM-A + ‖X‖² | GEMM-B (+ Ĝ(t+1)) | Gram(G_new) and
+    // Gram(Ĝ(t+1)) on all warps | warp 0: rates, reductions, state machine of t
+    // while warps 1.. run the receiver / weight update K1(t+1) of the next
+    // iteration.  K1(t+1) needs the stage flag of t+1, which the state machine
+    // of t decides: it is speculated (latched, or unchanged) and K1(t+1) is
+    // recomputed from the same inputs when the speculation was wrong (at most
+    // at the stage switch).  Results are identical to the sequential order:
+    // K1(t+1) reads only Ĝ(t+1), W(t) and the stage flag.  U/W/f terms are
+    // double-buffered by iteration parity.  5 block barriers per iteration.
     for (int t = 1; t <= a.max_iters; ++t) {
       const int cur = ctl.cur, oth = 1 - cur;
-      // stage test (solvers.py:449-459), evaluated redundantly by every thread
-      // from the shared state; the latch is committed at the end of the iteration
-      bool wn;
-      if (ctl.latched) {
-        wn = true;
-      } else {
-        double rs = INFINITY;
-        if (ctl.nhist >= 2) {
-          const double den = fabs(ctl.wsr_prev);
-          rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
+      const int bk = t & 1;  // bank holding K1(t)'s U / W / f terms
+      {  // update_weight_matrices raised inside iteration t (solvers.py:455-460)
+        const int lane = tid & 31;
+        int f1 = K;
+        for (int k = lane; k < K; k += 32)
+          if (f1 == K && e.ustat[k] != 0.0) f1 = k;
+        f1 = __reduce_min_sync(0xffffffffu, f1);
+        if (f1 < K) {
+          if (tid == 0) {
+            if (!ctl.latched && wn) {
+              if (a.latch) ctl.latched = 1;
+              if (ctl.switch_it < 0) ctl.switch_it = t;
+            }
+            ctl.status = (int)e.ustat[f1];
+            ctl.stop = 1;
+          }
+          break;
         }
-        wn = rs <= a.eps1;
       }
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
       pc.mark(0);
-      e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, wn, true);
+      e.build_yhat(e.Gr[oth], e.Gi[oth], ldg, K, KD);
       __syncthreads();
       pc.mark(1);
       // X = V̂ − γ ∇ into V[oth] (unscaled), ‖X‖² partials (solvers.py:358-377)
@@ -922,37 +970,41 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       e.gemm_hv(oth, oth, cur, ctl.omega, scale);
       __syncthreads();
       pc.mark(3);
-      {  // Gram(G_new) on all warps
+      const bool more = t < a.max_iters;
+      {  // Gram(G_new) -> gramb[1] and Gram(Ĝ(t+1)) -> gramb[0], all warps
         const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-        for (int k = warp; k < K; k += nw) e.gram_user(k, e.Gr[oth], e.Gi[oth], ldg, KD, lane);
+        const int ntask = more ? 2 * K : K;
+        for (int i = warp; i < ntask; i += nw) {
+          if (i < K)
+            e.gram_user(i, e.Gr[oth], e.Gi[oth], ldg, KD, lane, e.gramb[1]);
+          else
+            e.gram_user(i - K, e.Gr[cur], e.Gi[cur], ldg, KD, lane, e.gramb[0]);
+        }
       }
+      // speculated stage flag of t+1: read before the barrier (thread 0 updates
+      // ctl.latched in the next phase)
+      const bool wn_spec = ctl.latched || wn;
       __syncthreads();
       pc.mark(4);
-      if (K > 32) {
-        for (int k = tid; k < K; k += blockDim.x) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
-        __syncthreads();
-      }
       if (tid < 32) {  // warp 0: rates (lanes = users), reductions, state machine
         const int lane = tid;
-        if (K <= 32) {
-          if (lane < K) e.wsr_user(lane, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2);
-          __syncwarp();
-        }
+        for (int k = lane; k < K; k += 32) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, bk);
+        __syncwarp();
+        const double* fu = e.fub[bk];
+        const double* fw = e.fwb[bk];
         double su = 0.0, sw = 0.0, sr = 0.0, sv = 0.0;
-        int f1 = K, f2 = K;  // first user with a nonzero status (k1 / wsr)
+        int f2 = K;  // first user with a nonzero rate status
         for (int k = lane; k < K; k += 32) {
-          su += e.fu[k];
-          sw += e.fw[k];
+          su += fu[k];
+          sw += fw[k];
           sr += e.rate[k];
           sv += e.fv[k];
-          if (f1 == K && e.ustat[k] != 0.0) f1 = k;
           if (f2 == K && e.ust2[k] != 0.0) f2 = k;
         }
         su = warp_allsum(su);
         sw = warp_allsum(sw);
         sr = warp_allsum(sr);
         sv = warp_allsum(sv);
-        f1 = __reduce_min_sync(0xffffffffu, f1);
         f2 = __reduce_min_sync(0xffffffffu, f2);
         if (lane == 0) {
           if (!ctl.latched && wn) {
@@ -961,10 +1013,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
           }
           ctl.f_u = su;
           ctl.f_w = sw;
-          if (f1 < K) {  // update_weight_matrices raised inside iteration t
-            ctl.status = (int)e.ustat[f1];
-            ctl.stop = 1;
-          } else {
+          {
             const double wsr = sr;
             int st = f2 < K ? (int)e.ust2[f2] : 0;
             const double total_power = scale == 1.0 ? power : power * scale * scale;
@@ -1013,14 +1062,25 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
               }
             }
           }
+          ctl.wn_next = stage_flag();
         }
+      } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
+        for (int k = tid - 32; k < K; k += blockDim.x - 32)
+          e.k1_user(k, e.Gr[cur], e.Gi[cur], ldg, ctl.sigma2, wn_spec, true, bk, bk ^ 1);
       }
       __syncthreads();
       pc.mark(5);
       if (ctl.stop) break;
+      wn = ctl.wn_next != 0;
+      if (more && wn != wn_spec) {  // mis-speculated stage flag: redo K1(t+1)
+        for (int k = tid; k < K; k += blockDim.x)
+          e.k1_user(k, e.Gr[cur], e.Gi[cur], ldg, ctl.sigma2, wn, true, bk, bk ^ 1);
+        __syncthreads();
+      }
     }
 
     // ---------------- exit: stationarity residual (solvers.py:400-412, :507-509) ----------------
+    __syncthreads();  // thread 0's stop / status writes
     double residual = NAN;
     if (ctl.status == 0) {
       const int cur = ctl.cur, oth = 1 - cur;
@@ -1031,7 +1091,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
         e.Gi[oth][o] = e.Gi[cur][o];
       }
       __syncthreads();
-      e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, weighted, false);
+      e.phase_k1_yhat(e.Gr[oth], e.Gi[oth], ctl.sigma2, weighted, false, 0, 1);
       __syncthreads();
       if (tid == 0) {
         int st = 0;

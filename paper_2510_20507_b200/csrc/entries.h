@@ -10,6 +10,7 @@ struct KernelEntry {
   size_t (*smem_bytes)(int M, int K);          // Layout<R, N, d>::bytes
   const void* cluster_solve;                   // ammmse_cluster_kernel<R, N, d> (1 cluster / realization)
   size_t (*cluster_smem_bytes)(int M, int K, int C, int hres, int vglob, int sb, int tc);  // CLayout::bytes
+  const void* cluster_solve_tc;                // ammmse_cluster_kernel<float, N, d, true> (nullptr for fp64)
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4

@@ -18,13 +18,13 @@ size_t smem_fn(int M, int K) {
 }
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<double, 1, 1>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<1>,
-     (const void*)ammmse_cluster_kernel<double, 1, 1>, cluster_smem_fn<1>},
+     (const void*)ammmse_cluster_kernel<double, 1, 1>, cluster_smem_fn<1>, nullptr},
     {(const void*)ammmse_solve_kernel<double, 1, 2>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<2>,
-     (const void*)ammmse_cluster_kernel<double, 1, 2>, cluster_smem_fn<2>},
+     (const void*)ammmse_cluster_kernel<double, 1, 2>, cluster_smem_fn<2>, nullptr},
     {(const void*)ammmse_solve_kernel<double, 1, 3>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<3>,
-     (const void*)ammmse_cluster_kernel<double, 1, 3>, cluster_smem_fn<3>},
+     (const void*)ammmse_cluster_kernel<double, 1, 3>, cluster_smem_fn<3>, nullptr},
     {(const void*)ammmse_solve_kernel<double, 1, 4>, (const void*)ammmse_bounds_kernel<double, 1>, smem_fn<4>,
-     (const void*)ammmse_cluster_kernel<double, 1, 4>, cluster_smem_fn<4>},
+     (const void*)ammmse_cluster_kernel<double, 1, 4>, cluster_smem_fn<4>, nullptr},
 };
 }  // namespace
 const KernelEntry* entries_double_1() { return kEntries; }

@@ -18,13 +18,13 @@ size_t smem_fn(int M, int K) {
 }
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>,
-     (const void*)ammmse_cluster_kernel<float, 2, 1>, cluster_smem_fn<1>},
+     (const void*)ammmse_cluster_kernel<float, 2, 1>, cluster_smem_fn<1>, (const void*)ammmse_cluster_kernel<float, 2, 1, true>},
     {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>,
-     (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>},
+     (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>, (const void*)ammmse_cluster_kernel<float, 2, 2, true>},
     {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>,
-     (const void*)ammmse_cluster_kernel<float, 2, 3>, cluster_smem_fn<3>},
+     (const void*)ammmse_cluster_kernel<float, 2, 3>, cluster_smem_fn<3>, (const void*)ammmse_cluster_kernel<float, 2, 3, true>},
     {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>,
-     (const void*)ammmse_cluster_kernel<float, 2, 4>, cluster_smem_fn<4>},
+     (const void*)ammmse_cluster_kernel<float, 2, 4>, cluster_smem_fn<4>, (const void*)ammmse_cluster_kernel<float, 2, 4, true>},
 };
 }  // namespace
 const KernelEntry* entries_float_2() { return kEntries; }

@@ -18,13 +18,13 @@ size_t smem_fn(int M, int K) {
 }
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<float, 3, 1>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<1>,
-     (const void*)ammmse_cluster_kernel<float, 3, 1>, cluster_smem_fn<1>},
+     (const void*)ammmse_cluster_kernel<float, 3, 1>, cluster_smem_fn<1>, (const void*)ammmse_cluster_kernel<float, 3, 1, true>},
     {(const void*)ammmse_solve_kernel<float, 3, 2>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<2>,
-     (const void*)ammmse_cluster_kernel<float, 3, 2>, cluster_smem_fn<2>},
+     (const void*)ammmse_cluster_kernel<float, 3, 2>, cluster_smem_fn<2>, (const void*)ammmse_cluster_kernel<float, 3, 2, true>},
     {(const void*)ammmse_solve_kernel<float, 3, 3>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<3>,
-     (const void*)ammmse_cluster_kernel<float, 3, 3>, cluster_smem_fn<3>},
+     (const void*)ammmse_cluster_kernel<float, 3, 3>, cluster_smem_fn<3>, (const void*)ammmse_cluster_kernel<float, 3, 3, true>},
     {(const void*)ammmse_solve_kernel<float, 3, 4>, (const void*)ammmse_bounds_kernel<float, 3>, smem_fn<4>,
-     (const void*)ammmse_cluster_kernel<float, 3, 4>, cluster_smem_fn<4>},
+     (const void*)ammmse_cluster_kernel<float, 3, 4>, cluster_smem_fn<4>, (const void*)ammmse_cluster_kernel<float, 3, 4, true>},
 };
 }  // namespace
 const KernelEntry* entries_float_3() { return kEntries; }

@@ -72,23 +72,15 @@ __device__ __forceinline__ void k1_math_22(const cd (&Tg)[2][2], const cd (&G)[2
       T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
     }
   cd E[2][2];
-  if (want_f) {  // E = I - U^H G - G^H U + U^H A U
-    cd AU[2][2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      AU[0][s] = cadd(cscale(o.U[0][s], A.a), cmul(A.b, o.U[1][s]));
-      AU[1][s] = cadd(cmul(cconj(A.b), o.U[0][s]), cscale(o.U[1][s], A.c));
-    }
+  if (want_f) {
+    // At the MMSE receiver U = A^{-1} G:  U^H A U = U^H G, so the MSE matrix
+    // E = I - U^H G - G^H U + U^H A U  reduces to  I - G^H U = T^H  (T is
+    // Hermitian there up to rounding; its Hermitian part is used).
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        cd uau = cmk(0.0);
-        cfmac(uau, o.U[0][p], AU[0][q]);
-        cfmac(uau, o.U[1][p], AU[1][q]);
-        const cd ghu = cconj(csub(cmk(p == q ? 1.0 : 0.0), T[q][p]));
-        E[p][q] = cadd(csub(T[p][q], ghu), uau);
-      }
+      for (int q = 0; q < 2; ++q)
+        E[p][q] = cmk(0.5 * (T[p][q].r + T[q][p].r), 0.5 * (T[p][q].i - T[q][p].i));
     double tr = 0.0;
 #pragma unroll
     for (int p = 0; p < 2; ++p)
@@ -254,29 +246,15 @@ __device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[
       for (int a = 0; a < NN; ++a) cfmac(s, o.U[a][p], Gkk[a][q]);
       T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
     }
-  // MSE matrix in Gram form: E = I − U^H G_kk − G_kk^H U + U^H A U
+  // MSE matrix E = I − U^H G_kk − G_kk^H U + U^H A U at the MMSE receiver:
+  // U^H A U = U^H G_kk, so E = T^H (Hermitian part used, as in the 2x2 path)
   cd E[DD][DD];
   if (want_f) {
-    cd AU[NN][DD];
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int s = 0; s < DD; ++s) {
-        cd acc = cmk(0.0);
-#pragma unroll
-        for (int b = 0; b < NN; ++b) cfma(acc, A[a][b], o.U[b][s]);
-        AU[a][s] = acc;
-      }
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
-      for (int q = 0; q < DD; ++q) {
-        cd uau = cmk(0.0);
-#pragma unroll
-        for (int a = 0; a < NN; ++a) cfmac(uau, o.U[a][p], AU[a][q]);
-        const cd ghu = cconj(csub(cmk(p == q ? 1.0 : 0.0), T[q][p]));
-        E[p][q] = cadd(csub(T[p][q], ghu), uau);
-      }
+      for (int q = 0; q < DD; ++q)
+        E[p][q] = cmk(0.5 * (T[p][q].r + T[q][p].r), 0.5 * (T[p][q].i - T[q][p].i));
     double tr = 0.0;  // Tr(W_prev E): f_after_u uses the previous W (solvers.py:447)
 #pragma unroll
     for (int p = 0; p < DD; ++p)
@@ -288,40 +266,45 @@ __device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[
   }
   o.lndetw = 0.0;
   if (weighted) {
-    cd Tc[DD][DD], Ti[DD][DD];
+    // W = herm(T^{-1}) (np.linalg.solve(T, I) then hermitianize, linalg.py:12-14).
+    // T's anti-Hermitian part is rounding-level at the MMSE point, and
+    // herm(T^{-1}) = herm(T)^{-1} to second order in it, so W is formed from
+    // one Cholesky factorisation of herm(T): W = L^{-H} L^{-1}.  The same
+    // factor gives ln det W = -ln det herm(T) and the PD test of W
+    // (eigvalsh(W)[0] > 0, solvers.py:249-252): W is PD iff herm(T) is.
+    cd LT[DD][DD];
     double nT = 0.0;
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q) {
-        Tc[p][q] = T[p][q];
         nT += cabs2(T[p][q]);
+        LT[p][q] = cmk(0.5 * (T[p][q].r + T[q][p].r), 0.5 * (T[p][q].i - T[q][p].i));
       }
-    const bool ok = inverse_gj<DD>(Tc, Ti);  // np.linalg.solve(T, I)
-    double nTi = 0.0;
+    const bool pd = chol_lower<DD>(LT);
+    cd Ti[DD][DD];
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
-      for (int q = 0; q < DD; ++q) nTi += cabs2(Ti[p][q]);
+      for (int q = 0; q < DD; ++q) Ti[p][q] = cmk(p == q ? 1.0 : 0.0);
+    double nTi = 0.0;
+    if (pd) {
+      chol_solve<DD, DD>(LT, Ti);
+#pragma unroll
+      for (int p = 0; p < DD; ++p)
+#pragma unroll
+        for (int q = 0; q < DD; ++q) nTi += cabs2(Ti[p][q]);
+    }
     // ‖T‖_F ‖T^{-1}‖_F: an upper bound (within a factor d) of np.linalg.cond
     const double cond = sqrt(nT) * sqrt(nTi);
-    if ((!ok || !isfinite(cond) || cond > kCondLimitUA) && o.status == 0)
+    if ((!pd || !isfinite(cond) || cond > kCondLimitUA) && o.status == 0)
       o.status = AMMMSE_STATUS_ILL_CONDITIONED;
 #pragma unroll
-    for (int p = 0; p < DD; ++p)  // hermitianize (linalg.py:12-14)
+    for (int p = 0; p < DD; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q)
         o.W[p][q] = cmk(0.5 * (Ti[p][q].r + Ti[q][p].r), 0.5 * (Ti[p][q].i - Ti[q][p].i));
-    cd LW[DD][DD];
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) LW[p][q] = o.W[p][q];
-    if (!chol_lower<DD>(LW)) {  // eigvalsh(W)[0] <= 0 (solvers.py:249-252)
-      if (o.status == 0) o.status = AMMMSE_STATUS_ILL_CONDITIONED;
-    } else {
-      o.lndetw = chol_lndet<DD>(LW);
-    }
+    if (pd) o.lndetw = -chol_lndet<DD>(LT);
   } else {
 #pragma unroll
     for (int p = 0; p < DD; ++p)
