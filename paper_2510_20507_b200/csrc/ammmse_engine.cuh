@@ -131,10 +131,11 @@ struct Layout {
   //   alpha, fv, rate  K each
   //   ustat, ust2  K each (k1 / wsr per-user status, stored as double)
   //   red    32
-  __host__ __device__ size_t dbl_count() const {
-    return (size_t)2 * (2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + 3 * K) + 3 * K +
-           2 * K + 32;
+  // doubles per bank, rounded even so both banks keep 16-byte cd alignment
+  __host__ __device__ size_t bank_doubles() const {
+    return ((size_t)2 * K * NN * NN + 2 * K * NN * DD + 2 * K * DD * DD + 3 * K + 1) & ~(size_t)1;
   }
+  __host__ __device__ size_t dbl_count() const { return 2 * bank_doubles() + 3 * K + 2 * K + 32; }
   __host__ __device__ size_t dbl_bytes() const { return dbl_count() * sizeof(double); }
 };
 
@@ -460,15 +461,30 @@ __device__ __forceinline__ void user_grams(const R* __restrict__ Xr, const R* __
 // ---------------------------------------------------------------------------
 // The solver kernel
 // ---------------------------------------------------------------------------
+// Two equally spaced buffers addressed by a runtime index (no pointer array
+// in local memory): view[i] = base + i * stride.
+template <typename T>
+struct Pair {
+  T* base;
+  size_t stride;
+  __device__ __forceinline__ T* operator[](int i) const { return base + (size_t)i * stride; }
+};
+
+// Operands that live in shared memory: lets the compiler emit LDS/STS with
+// 32-bit addresses instead of generic 64-bit LD/ST.  Only for pointers that
+// are never null.
+#define AMMMSE_SHARED(p) __builtin_assume(__isShared(p))
+
 template <typename R, int NN, int DD>
 struct Engine {
   using L_t = Layout<R, NN, DD>;
 
   // smem views
-  R *Hr, *Hi, *Vr[2], *Vi[2], *Gr[2], *Gi[2];
+  R *Hr, *Hi;
+  Pair<R> Vr, Vi, Gr, Gi;
   RC<R>*Uf, *Pf, *Df;  // per user N x d, R
-  cd *gramb[2], *ucb[2], *wcb[2];
-  double *lndb[2], *fub[2], *fwb[2];
+  Pair<cd> gramb, ucb, wcb;
+  Pair<double> lndb, fub, fwb;
   double *alpha, *fv, *rate, *ustat, *ust2, *red;
   L_t L;
 
@@ -477,21 +493,26 @@ struct Engine {
     R* base = reinterpret_cast<R*>(smem);
     Hr = base + L.oH;
     Hi = Hr + L.nH;
-    Vr[0] = base + L.oV0; Vi[0] = Vr[0] + L.nV;
-    Vr[1] = base + L.oV1; Vi[1] = Vr[1] + L.nV;
-    Gr[0] = base + L.oG0; Gi[0] = Gr[0] + L.nG;
-    Gr[1] = base + L.oG1; Gi[1] = Gr[1] + L.nG;
+    // V[1] follows V[0] (re, im planes) and G[1] follows G[0]: see Layout
+    Vr = Pair<R>{base + L.oV0, L.oV1 - L.oV0};
+    Vi = Pair<R>{base + L.oV0 + L.nV, L.oV1 - L.oV0};
+    Gr = Pair<R>{base + L.oG0, L.oG1 - L.oG0};
+    Gi = Pair<R>{base + L.oG0 + L.nG, L.oG1 - L.oG0};
     Uf = reinterpret_cast<RC<R>*>(base + L.oUPD);
     Pf = Uf + K * NN * DD;
     Df = Pf + K * NN * DD;
     double* d = reinterpret_cast<double*>(smem + L.dbl_off);
-    for (int b = 0; b < 2; ++b) {
-      gramb[b] = reinterpret_cast<cd*>(d); d += 2 * K * NN * NN;
-      ucb[b] = reinterpret_cast<cd*>(d); d += 2 * K * NN * DD;
-      wcb[b] = reinterpret_cast<cd*>(d); d += 2 * K * DD * DD;
-      lndb[b] = d; d += K;
-      fub[b] = d; d += K;
-      fwb[b] = d; d += K;
+    {  // bank b of each array at + b * bank (doubles)
+      const size_t bank = L.bank_doubles();
+      const size_t bank_cd = bank / 2;
+      double* const d0 = d;
+      gramb = Pair<cd>{reinterpret_cast<cd*>(d), bank_cd}; d += 2 * K * NN * NN;
+      ucb = Pair<cd>{reinterpret_cast<cd*>(d), bank_cd}; d += 2 * K * NN * DD;
+      wcb = Pair<cd>{reinterpret_cast<cd*>(d), bank_cd}; d += 2 * K * DD * DD;
+      lndb = Pair<double>{d, bank}; d += K;
+      fub = Pair<double>{d, bank}; d += K;
+      fwb = Pair<double>{d, bank}; d += K;
+      d = d0 + 2 * bank;
     }
     alpha = d; d += K;
     fv = d; d += K;
@@ -511,6 +532,17 @@ struct Engine {
     const cd* wprev = wcb[bin];
     cd* ucache = ucb[bout];
     cd* wcache = wcb[bout];
+    AMMMSE_SHARED(gram);
+    AMMMSE_SHARED(wprev);
+    AMMMSE_SHARED(ucache);
+    AMMMSE_SHARED(wcache);
+    AMMMSE_SHARED(Gwr);
+    AMMMSE_SHARED(Gwi);
+    AMMMSE_SHARED(Df);
+    AMMMSE_SHARED(Uf);
+    AMMMSE_SHARED(Pf);
+    AMMMSE_SHARED(alpha);
+    AMMMSE_SHARED(ustat);
     cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -555,6 +587,15 @@ struct Engine {
     const cd* gram = gramb[1];
     const cd* ucache = ucb[b];
     const cd* wcache = wcb[b];
+    AMMMSE_SHARED(gram);
+    AMMMSE_SHARED(ucache);
+    AMMMSE_SHARED(wcache);
+    AMMMSE_SHARED(Gnr);
+    AMMMSE_SHARED(Gni);
+    AMMMSE_SHARED(alpha);
+    AMMMSE_SHARED(rate);
+    AMMMSE_SHARED(fv);
+    AMMMSE_SHARED(ust2);
     cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -584,6 +625,9 @@ struct Engine {
   // columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
   __device__ void gram_user(int k, const R* __restrict__ Xr, const R* __restrict__ Xi, int ld,
                             int ncols, int lane, cd* gram) {
+    AMMMSE_SHARED(Xr);
+    AMMMSE_SHARED(Xi);
+    AMMMSE_SHARED(gram);
     double sr[NN][NN], si[NN][NN];
 #pragma unroll
     for (int a = 0; a < NN; ++a)
@@ -692,6 +736,11 @@ struct Engine {
 
   // Ŷ in place over the work G: (m, j) pairs, j fastest.
   __device__ void build_yhat(R* Gwr, R* Gwi, int ldg, int K, int KD) {
+    AMMMSE_SHARED(Gwr);
+    AMMMSE_SHARED(Gwi);
+    AMMMSE_SHARED(Df);
+    AMMMSE_SHARED(Uf);
+    AMMMSE_SHARED(Pf);
     for (int idx = threadIdx.x; idx < K * KD; idx += blockDim.x) {
       const int m = idx / KD, j = idx - m * KD;
       const int b = j / DD, s = j - b * DD;
@@ -755,6 +804,8 @@ struct Engine {
     R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
     const R om = (R)omega, sc = (R)vscale;
     const int ldg = L.ldg;
+    AMMMSE_SHARED(gr);
+    AMMMSE_SHARED(gi);
     cgemm_any<R, 2, 4, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
                                [&](int p, int q, R cr, R ci) {
                                  const int o = p * ldg + q;
@@ -763,6 +814,8 @@ struct Engine {
                                  gr[o] = cr;
                                  gi[o] = ci;
                                  if (hr) {
+                                   AMMMSE_SHARED(hr);
+                                   AMMMSE_SHARED(hi);
                                    hr[o] = cr + om * (cr - hr[o]);
                                    hi[o] = ci + om * (ci - hi[o]);
                                  }
@@ -780,6 +833,11 @@ struct Engine {
     const R* vci = Vi[vcur];
     R* xr = Vr[dst];
     R* xi = Vi[dst];
+    AMMMSE_SHARED(vcr);
+    AMMMSE_SHARED(vci);
+    AMMMSE_SHARED(xr);
+    AMMMSE_SHARED(xi);
+    AMMMSE_SHARED(red);
     const int ldv = L.ldv;
     const R st = (R)step, om = (R)omega, sc = (R)sc_cur, so = (R)sc_old;
     double pw = 0.0;
