@@ -329,9 +329,16 @@ __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R*
   __builtin_assume(__isShared(Br));
   __builtin_assume(__isShared(Bi));
   const int QT = Q / RX, tiles = (P / RY) * QT;
-  const int w = threadIdx.x;
-  const bool active = w < tiles * S;
-  const int tile = active ? w / S : 0, s = w - (w / S) * S;
+  // split-major lanes: a warp holds 32/S consecutive tiles, and the K split s
+  // is the high part of the lane index, so every quarter-warp (the unit a
+  // 128-bit shared load is serviced in) reads one K slice of consecutive
+  // tiles: broadcast A, contiguous B, no bank conflicts between K slices
+  // whose rows alias (row stride = 0 mod 32 words).
+  const int lane = threadIdx.x & 31, tpw = 32 / S;
+  const int s = lane / tpw;
+  const int tile_raw = (threadIdx.x >> 5) * tpw + (lane - s * tpw);
+  const bool active = tile_raw < tiles;
+  const int tile = active ? tile_raw : 0;
   const int p0 = (tile / QT) * RY, q0 = (tile % QT) * RX;
   const int kper = KD / S, kb = s * kper;
   R cr[RY][RX], ci[RY][RX];
@@ -378,8 +385,8 @@ __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R*
       }
     }
   }
-  // split-K reduction over the S adjacent lanes of a tile (S | 32, aligned)
-  for (int o = 1; o < S; o <<= 1) {
+  // split-K reduction over the S lanes of a tile (lane bits >= log2(32/S))
+  for (int o = tpw; o < 32; o <<= 1) {
 #pragma unroll
     for (int i = 0; i < RY; ++i)
 #pragma unroll
