@@ -52,11 +52,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <typename R, int RY, int RX, int TPT, bool CONJT, class Epi>
+struct NoPre {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `pre()` runs after the K loop, once the staging ring is free and before the
+// epilogue (all threads): used to stage epilogue operands that live in global
+// memory into the ring (V_old with h_placement 3).
+template <typename R, int RY, int RX, int TPT, bool CONJT, class Epi, class Pre = NoPre>
 __device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* __restrict__ Hg,
                                              int ldH, RC<R>* __restrict__ stage, int SB,
                                              const R* __restrict__ Br, const R* __restrict__ Bi,
-                                             int ldb, Epi epi) {
+                                             int ldb, Epi epi, Pre pre = Pre()) {
   constexpr int EPC = 16 / sizeof(RC<R>);  // complex elements per 16-byte piece (2 or 1)
   // chunk extent along k; !CONJT rows are padded by EPC elements (bank spread,
   // 16-byte aligned row starts), so P * (KC + EPC) <= SB
@@ -144,6 +151,7 @@ __device__ __forceinline__ void cgemm_stream(int P, int Q, int KD, const RC<R>* 
     }
     __syncthreads();  // buffer (c & 1) may be refilled by the next issue
   }
+  pre();
 #pragma unroll
   for (int t = 0; t < TPT; ++t) {
     const int tile = threadIdx.x + t * blockDim.x;
@@ -192,20 +200,19 @@ __host__ __device__ inline bool stream2_ok(int P, int Q, int KD, int ldb, int SB
   return true;
 }
 
-template <typename R, int RY, int RX, int NST, bool CONJT, class Epi>
+template <typename R, int RY, int RX, int NST, bool CONJT, class Epi, class Pre = NoPre>
 __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>* __restrict__ Hg,
                                               int ldH, RC<R>* __restrict__ stage, int SB,
                                               const R* __restrict__ Br, const R* __restrict__ Bi,
-                                              int ldb, Epi epi) {
+                                              int ldb, Epi epi, Pre pre = Pre()) {
   constexpr int EPC = 16 / sizeof(RC<R>);  // complex per 16-byte piece
   const int KC = stream2_kc<R>(CONJT, P, SB);
   const int lds = CONJT ? P : KC + EPC;
   const int nchunks = (KD + KC - 1) / KC;
-  if constexpr (RY <= 4) {  // operands in shared memory -> LDS (measured slower for 8-row tiles)
-    __builtin_assume(__isShared(stage));
-    __builtin_assume(__isShared(Br));
-    __builtin_assume(__isShared(Bi));
-  }
+  // operands in shared memory -> LDS (generic LD would sit on the long scoreboard)
+  __builtin_assume(__isShared(stage));
+  __builtin_assume(__isShared(Br));
+  __builtin_assume(__isShared(Bi));
   const int QT = Q / RX, ntiles = (P / RY) * QT;
   const bool active = threadIdx.x < ntiles;
   const int tile = active ? threadIdx.x : 0;
@@ -311,6 +318,7 @@ __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>*
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();  // ring free for the next GEMM
+  pre();
   if (active) {
 #pragma unroll
     for (int i = 0; i < RY; ++i)
@@ -385,12 +393,13 @@ struct CLayout {
     dbl_off = ((nR * sizeof(R)) + 15) & ~(size_t)15;
     bytes = dbl_off + dbl_count() * sizeof(double);
   }
-  // fp64 region: gx[2] (K*NN*NN cd each), ucache (KL*NN*DD cd), wcache
-  // (KL*DD*DD cd), lndetw, alpha_own, fu, fw, fv, rate, ust (KL each),
-  // xs (XS_COUNT), red (32)
+  // fp64 region: gx[2] (K*NN*NN cd each), ucache[2] (KL*NN*DD cd each),
+  // wcache[2] (KL*DD*DD cd each), lndetw[2], alpha_own, fu, fw, fv, rate,
+  // ust, ust2 (KL each), xs (XS_COUNT), red (32).  [2] = bank by iteration
+  // parity: WSR(t) and K1(t+1) run concurrently.
   __host__ __device__ size_t dbl_count() const {
-    return (size_t)2 * 2 * K * NN * NN + 2 * KL * NN * DD + 2 * KL * DD * DD + 7 * KL + XS_COUNT +
-           32;
+    return (size_t)2 * 2 * K * NN * NN + 2 * 2 * KL * NN * DD + 2 * 2 * KL * DD * DD + 9 * KL +
+           XS_COUNT + 32;
   }
 };
 
@@ -436,15 +445,19 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   cd* gx[2];
   gx[0] = reinterpret_cast<cd*>(dp); dp += 2 * K * NN * NN;
   gx[1] = reinterpret_cast<cd*>(dp); dp += 2 * K * NN * NN;
-  cd* ucache = reinterpret_cast<cd*>(dp); dp += 2 * KL * NN * DD;
-  cd* wcache = reinterpret_cast<cd*>(dp); dp += 2 * KL * DD * DD;
-  double* lndetw = dp; dp += KL;
+  const Pair<cd> ucb{reinterpret_cast<cd*>(dp), (size_t)KL * NN * DD};  // bank b: ucb[b]
+  dp += 2 * 2 * KL * NN * DD;
+  const Pair<cd> wcb{reinterpret_cast<cd*>(dp), (size_t)KL * DD * DD};
+  dp += 2 * 2 * KL * DD * DD;
+  const Pair<double> lndb{dp, (size_t)KL};
+  dp += 2 * KL;
   double* alpha = dp; dp += KL;
   double* fu = dp; dp += KL;
   double* fw = dp; dp += KL;
   double* fv = dp; dp += KL;
   double* rate = dp; dp += KL;
   double* ust = dp; dp += KL;
+  double* ust2 = dp; dp += KL;
   double* xs = dp; dp += XS_COUNT;
   double* red = dp;
 
@@ -512,9 +525,15 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         for (int q = 0; q < NN; ++q) Tg[p][q] = cadd(Tg[p][q], g[p * NN + q]);
     }
   };
-  // one pass of per-user K1 for the own users + U/P publication
-  auto k1_phase = [&](int gsrc, bool weighted, bool want_f) {
-    for (int kl = tid; kl < KL; kl += blockDim.x) {
+  // per-user K1 of own users kl = first, first + step, ... from the reduced
+  // Gram gx[0] and the work Ĝ in G[gsrc]; W_prev / ln det W_prev from bank
+  // bin, U / W / ln det W to bank bout (solvers.py:210-254)
+  auto k1_users = [&](int gsrc, bool weighted, bool want_f, int bin, int bout, int first,
+                      int step) {
+    const cd* wprev = wcb[bin];
+    cd* ucache = ucb[bout];
+    cd* wcache = wcb[bout];
+    for (int kl = first; kl < KL; kl += step) {
       cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
       gram_of(0, kl, Tg);
 #pragma unroll
@@ -527,9 +546,9 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
 #pragma unroll
       for (int p = 0; p < DD; ++p)
 #pragma unroll
-        for (int q = 0; q < DD; ++q) Wp[p][q] = wcache[(kl * DD + p) * DD + q];
+        for (int q = 0; q < DD; ++q) Wp[p][q] = wprev[(kl * DD + p) * DD + q];
       K1Out<NN, DD> o;
-      k1_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], Wp, lndetw[kl], weighted, want_f, o);
+      k1_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], Wp, lndb[bin][kl], weighted, want_f, o);
 #pragma unroll
       for (int p = 0; p < NN; ++p)
 #pragma unroll
@@ -544,26 +563,27 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       for (int p = 0; p < DD; ++p)
 #pragma unroll
         for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = o.W[p][q];
-      lndetw[kl] = o.lndetw;
+      lndb[bout][kl] = o.lndetw;
       fu[kl] = o.fu;
       fw[kl] = o.fw;
       ust[kl] = o.status;
     }
-    __syncthreads();
-    if (tid == 0) {
-      double su = 0.0, sw = 0.0;
-      int st = 0;
-      for (int kl = 0; kl < KL; ++kl) {
-        su += fu[kl];
-        sw += fw[kl];
-        if (st == 0 && ust[kl] != 0.0) st = (int)ust[kl];
-      }
-      xs[XS_FU] = su;
-      xs[XS_FW] = sw;
-      xs[XS_ST1] = st;
+  };
+  // per-CTA K1 sums -> exchange slots (one thread, after the K1 writes are visible)
+  auto k1_publish = [&]() {
+    double su = 0.0, sw = 0.0;
+    int st = 0;
+    for (int kl = 0; kl < KL; ++kl) {
+      su += fu[kl];
+      sw += fw[kl];
+      if (st == 0 && ust[kl] != 0.0) st = (int)ust[kl];
     }
-    cl.sync();
-    // gather the other owners' U and α U W
+    xs[XS_FU] = su;
+    xs[XS_FW] = sw;
+    xs[XS_ST1] = st;
+  };
+  // gather the other owners' U and α U W (after a cluster barrier)
+  auto k1_gather = [&]() {
     const int per = NN * DD;
     for (int i = tid; i < K * per; i += blockDim.x) {
       const int owner = (i / per) / KL;
@@ -572,6 +592,14 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         Pall[i] = cl.map_shared_rank(Pall, owner)[i];
       }
     }
+  };
+  // one non-overlapped K1 pass + publication + gather
+  auto k1_phase = [&](int gsrc, bool weighted, bool want_f, int bin, int bout) {
+    k1_users(gsrc, weighted, want_f, bin, bout, tid, blockDim.x);
+    __syncthreads();
+    if (tid == 0) k1_publish();
+    cl.sync();
+    k1_gather();
   };
   // Ŷ over own columns, in place over G[g]
   auto build_yhat = [&](int g) {
@@ -641,13 +669,31 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     R* xi = Vi[vx];
     const R st = (R)step, om = (R)omega;
     double pw = 0.0;
+    // V_old in global scratch (h_placement 3): staged into the free H ring
+    // after the K loop, so the epilogue reads it from shared memory
+    const bool stage_vold = extrap && L.vglob && vo == 1 && !hres &&
+                            L.nV <= (size_t)kStreamStages * L.SB &&
+                            (2 * L.nV * sizeof(R)) % 16 == 0;
+    const R* rdr = stage_vold ? reinterpret_cast<const R*>(stage) : vor;
+    const R* rdi = stage_vold ? rdr + L.nV : voi;
+    auto pre = [&]() {
+      if (stage_vold) {
+        const int n16 = (int)((2 * L.nV * sizeof(R)) / 16);
+        constexpr int per = 16 / (int)sizeof(R);
+        R* dst = reinterpret_cast<R*>(stage);
+        for (int i = tid; i < n16; i += blockDim.x) cp_async16(dst + i * per, vor + i * per);
+        cp_async_commit();
+        cp_async_wait0();
+        __syncthreads();
+      }
+    };
     auto epi = [&](int p, int q, R gr, R gi) {
       const int o = p * ldv + q;
       const R cr0 = vcr[o], ci0 = vci[o];
       R vr = cr0, vi = ci0;
       if (extrap) {
-        vr = vr + om * (vr - vor[o]);
-        vi = vi + om * (vi - voi[o]);
+        vr = vr + om * (vr - rdr[o]);
+        vi = vi + om * (vi - rdi[o]);
       }
       const R x_r = vr - st * gr, x_i = vi - st * gi;
       if (save) {
@@ -684,34 +730,50 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     else if ((M / 4) * (ncol / 4) < (int)blockDim.x &&
              stream2_ok<R, 2, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
       cgemm_stream2<R, 2, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
-                                                   Gi[ysrc], ldg, epi);
+                                                   Gi[ysrc], ldg, epi, pre);
     else if (stream2_ok<R, 4, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
       cgemm_stream2<R, 4, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
-                                                   Gi[ysrc], ldg, epi);
+                                                   Gi[ysrc], ldg, epi, pre);
     else if (stream2_ok<R, 8, 4, true>(M, ncol, KN, ldg, L.SB, blockDim.x))
       cgemm_stream2<R, 8, 4, kStreamStages, true>(M, ncol, KN, Hcur, M, stage, L.SB, Gr[ysrc],
-                                                   Gi[ysrc], ldg, epi);
+                                                   Gi[ysrc], ldg, epi, pre);
     else
       cgemm_stream<R, kStreamRY, kStreamRX, kStreamTPT, true>(M, ncol, KN, Hcur, M, stage, L.SB,
-                                                              Gr[ysrc], Gi[ysrc], ldg, epi);
+                                                              Gr[ysrc], Gi[ysrc], ldg, epi, pre);
     pw = block_sum(pw, red);
     if (tid == 0) xs[XS_POWER] = pw;
     cl.sync();
     return xsum(XS_POWER);
   };
-  auto gemm_hv = [&](int src, int dst) {
+  // GEMM-B: G[dst] = H V[src].  With ghat >= 0 the epilogue also writes the
+  // next iteration's extrapolated Ĝ = G + ω (G − G_prev) over G[ghat], which
+  // holds G_prev (solvers.py:380-390 by linearity).
+  auto gemm_hv = [&](int src, int dst, int ghat, double omega) {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
+    R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
+    R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
+    const R om = (R)omega;
     auto epi = [&](int p, int q, R cr, R ci) {
-      gr[p * ldg + q] = cr;
-      gi[p * ldg + q] = ci;
+      const int o = p * ldg + q;
+      gr[o] = cr;
+      gi[o] = ci;
+      if (hr) {  // ω = 0: plain copy (G_prev may be uninitialised shared memory)
+        hr[o] = om == R(0) ? cr : cr + om * (cr - hr[o]);
+        hi[o] = om == R(0) ? ci : ci + om * (ci - hi[o]);
+      }
     };
     if constexpr (sizeof(R) == 4) {
       if (TC && L.tc) {  // G = H V on tcgen05 (signs -,+)
         tcg::gemm<kTcStages>(ring, KN, ncol, M, hpB, (const float*)Vr[src], (const float*)Vi[src],
                              ldv, -1.f, 1.f);
         tcg::for_each_d(ring, KN, ncol, [&](int p, int q, int part, float g) {
-          (part ? gi : gr)[p * ldg + q] = g;
+          const int o = p * ldg + q;
+          (part ? gi : gr)[o] = g;
+          if (hr) {
+            R* h = part ? hi : hr;
+            h[o] = om == R(0) ? g : g + om * (g - h[o]);
+          }
         });
         umma::fence_before();
       }
@@ -770,9 +832,9 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       }
       for (int kl = tid; kl < KL; kl += blockDim.x) {
         alpha[kl] = a.alpha[(size_t)r * K + k0 + kl];
-        lndetw[kl] = 0.0;
+        lndb[0][kl] = 0.0;  // W_prev = I at t = 1 (solvers.py:429-430); K1(1) reads bank 0
         for (int p = 0; p < DD; ++p)
-          for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
+          for (int q = 0; q < DD; ++q) wcb[0][(kl * DD + p) * DD + q] = cmk(p == q ? 1.0 : 0.0);
       }
       if (tid == 0) {
         ctl.sigma2 = a.sigma2[r];
@@ -846,65 +908,58 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         if (crank == 0 && a.gamma_used) a.gamma_used[r] = ctl.gamma;
       }
     }
-    gemm_hv(0, 0);
+    // initial G = H V0 into G[0]; Ĝ(1) = G (no extrapolation at t = 1) into G[1]
+    gemm_hv(0, 0, 1, 0.0);
     __syncthreads();
 
-    // ---------------- main loop (solvers.py:440-505) ----------------
+    // Stage flag of iteration t (solvers.py:449-459), from the shared state.
+    auto stage_flag = [&]() -> bool {
+      if (ctl.latched) return true;
+      double rs = INFINITY;
+      if (ctl.nhist >= 2) {
+        const double den = fabs(ctl.wsr_prev);
+        rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
+      }
+      return rs <= a.eps1;
+    };
+    // ---------------- K1(1) (solvers.py:440-460 at t = 1) ----------------
+    bool wn = stage_flag();  // the flag K1(t) was computed with
+    gram_partials(Gr[1], Gi[1], 0);
+    cl.sync();
+    k1_phase(1, wn, true, 0, 1);
+    pc.mark(9);  // setup: load, bounds, G = H V0, K1(1)
+
+    // ---------------- main loop (solvers.py:440-505), software-pipelined ----------------
+    // Per iteration t: [K1(t) status] | Ŷ(t) | GEMM-A + ‖X‖² (cluster sum) |
+    // projection | GEMM-B (+ Ĝ(t+1) in its epilogue) | Gram partials of G_new
+    // and Ĝ(t+1) | warp 0: WSR(t) of own users while warps 1..: K1(t+1) with a
+    // speculated stage flag | exchange | every CTA: state machine of t (fixed
+    // rank order, identical decisions), K1(t+1) redone if mis-speculated, U/P
+    // gather.  U/W/ln det W double-buffered by iteration parity.  Three cluster
+    // barriers per iteration (four at a stage switch).
     for (int t = 1; t <= a.max_iters; ++t) {
       const int cur = ctl.cur, oth = 1 - cur;
-      if (tid == 0) {  // stage test (solvers.py:449-459), identical in every CTA
-        int wn;
-        if (ctl.latched) {
-          wn = 1;
-        } else {
-          double rs = INFINITY;
-          if (ctl.nhist >= 2) {
-            const double den = fabs(ctl.wsr_prev);
-            rs = den == 0.0 ? INFINITY : fabs(ctl.wsr_last - ctl.wsr_prev) / den;
-          }
-          wn = rs <= a.eps1;
-          if (wn) {
-            if (a.latch) ctl.latched = 1;
-            if (ctl.switch_it < 0) ctl.switch_it = t;
-          }
-        }
-        ctl.weighted_now = wn;
-      }
-      const bool extrap = (t >= 2) && (ctl.omega > 0.0);
-      pc.mark(0);
-      {
-        const R om = (R)ctl.omega;
-        R *gcr = Gr[cur], *gci = Gi[cur], *gwr = Gr[oth], *gwi = Gi[oth];
-        for (int i = tid; i < KN * ncol; i += blockDim.x) {
-          R xr = gcr[i], xi = gci[i];
-          if (extrap) {
-            xr = xr + om * (xr - gwr[i]);
-            xi = xi + om * (xi - gwi[i]);
-          }
-          gwr[i] = xr;
-          gwi[i] = xi;
-        }
-      }
-      __syncthreads();
-      gram_partials(Gr[oth], Gi[oth], 0);
-      cl.sync();
-      pc.mark(1);
-      k1_phase(oth, ctl.weighted_now, true);
-      if (tid == 0) {
+      const int bk = t & 1;  // bank holding K1(t)'s U / W / ln det W
+      if (tid == 0) {  // K1(t) results (published before the last cluster barrier)
         ctl.f_u = xsum(XS_FU);
         ctl.f_w = xsum(XS_FW);
         const int st = xfirst(XS_ST1);
-        if (st) {
+        if (st) {  // update_weight_matrices raised inside iteration t (solvers.py:455-460)
+          if (!ctl.latched && wn) {
+            if (a.latch) ctl.latched = 1;
+            if (ctl.switch_it < 0) ctl.switch_it = t;
+          }
           ctl.status = st;
           ctl.stop = 1;
         }
       }
+      const bool extrap = (t >= 2) && (ctl.omega > 0.0);
       __syncthreads();
-      pc.mark(2);
+      pc.mark(0);
       if (ctl.stop) break;
       build_yhat(oth);
       __syncthreads();
-      pc.mark(3);
+      pc.mark(1);
       const bool pin = L.vglob;  // current precoders pinned in SMEM slot 0
       const int vx = pin ? 0 : oth;
       const double power = pin ? grad_step(oth, 0, 1, 0, true, ctl.step, ctl.omega, extrap)
@@ -919,57 +974,82 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         }
       }
       __syncthreads();
-      pc.mark(4);
-      gemm_hv(vx, oth);
+      pc.mark(2);
+      const bool more = t < a.max_iters;
+      // G_new over Ŷ; Ĝ(t+1) over G_cur (which becomes G_old)
+      gemm_hv(vx, oth, more ? cur : -1, ctl.omega);
       __syncthreads();
-      pc.mark(5);
-      gram_partials(Gr[oth], Gi[oth], 1);
-      cl.sync();
-      pc.mark(6);
-      for (int kl = tid; kl < KL; kl += blockDim.x) {
-        cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
-        gram_of(1, kl, Tg);
-#pragma unroll
-        for (int p = 0; p < NN; ++p)
-#pragma unroll
-          for (int s = 0; s < DD; ++s) {
-            const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
-            Gkk[p][s] = cmk((double)Gr[oth][idx], (double)Gi[oth][idx]);
-            U[p][s] = ucache[(kl * NN + p) * DD + s];
-          }
-#pragma unroll
-        for (int p = 0; p < DD; ++p)
-#pragma unroll
-          for (int q = 0; q < DD; ++q) W[p][q] = wcache[(kl * DD + p) * DD + q];
-        double rr, ff;
-        int st;
-        wsr_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], U, W, lndetw[kl], rr, ff, st);
-        rate[kl] = rr;
-        fv[kl] = ff;
-        ust[kl] = st;
+      pc.mark(3);
+      {  // Gram partials of G_new -> gx[1] and of Ĝ(t+1) -> gx[0], all warps
+        const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+        for (int k = warp; k < K; k += nw)
+          gram_pair<R, NN>(k, Gr[oth], Gi[oth], gx[1], more ? Gr[cur] : nullptr, Gi[cur], gx[0],
+                           ldg, ncol, lane);
       }
-      __syncthreads();
-      if (tid == 0) {
+      // speculated stage flag of t+1 (thread 0 updates ctl.latched below)
+      const bool wn_spec = ctl.latched || wn;
+      cl.sync();
+      pc.mark(4);
+      if (tid < 32) {  // warp 0: rates / f_after_v of own users (lanes), CTA partials
+        const int lane = tid;
+        const cd* ucache = ucb[bk];
+        const cd* wcache = wcb[bk];
+        for (int kl = lane; kl < KL; kl += 32) {
+          cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
+          gram_of(1, kl, Tg);
+#pragma unroll
+          for (int p = 0; p < NN; ++p)
+#pragma unroll
+            for (int s = 0; s < DD; ++s) {
+              const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
+              Gkk[p][s] = cmk((double)Gr[oth][idx], (double)Gi[oth][idx]);
+              U[p][s] = ucache[(kl * NN + p) * DD + s];
+            }
+#pragma unroll
+          for (int p = 0; p < DD; ++p)
+#pragma unroll
+            for (int q = 0; q < DD; ++q) W[p][q] = wcache[(kl * DD + p) * DD + q];
+          double rr, ff;
+          int st;
+          wsr_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], U, W, lndb[bk][kl], rr, ff, st);
+          rate[kl] = rr;
+          fv[kl] = ff;
+          ust2[kl] = st;
+        }
+        __syncwarp();
         double sr = 0.0, sv = 0.0;
-        int st = 0;
-        for (int kl = 0; kl < KL; ++kl) {
+        int f2 = KL;
+        for (int kl = lane; kl < KL; kl += 32) {  // lane-strided, then a fixed shuffle tree
           sr += rate[kl];
           sv += fv[kl];
-          if (st == 0 && ust[kl] != 0.0) st = (int)ust[kl];
+          if (f2 == KL && ust2[kl] != 0.0) f2 = kl;
         }
-        xs[XS_RATE] = sr;
-        xs[XS_FV] = sv;
-        xs[XS_ST2] = st;
+        sr = warp_allsum(sr);
+        sv = warp_allsum(sv);
+        f2 = __reduce_min_sync(0xffffffffu, f2);
+        if (lane == 0) {
+          xs[XS_RATE] = sr;
+          xs[XS_FV] = sv;
+          xs[XS_ST2] = f2 < KL ? ust2[f2] : 0.0;
+        }
+      } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
+        k1_users(cur, wn_spec, true, bk, bk ^ 1, tid - 32, blockDim.x - 32);
       }
-      pc.mark(7);
+      __syncthreads();
+      if (more && tid == 32) k1_publish();
       cl.sync();
-      if (tid == 0) {
+      pc.mark(5);
+      if (tid == 0) {  // state machine of iteration t, identical in every CTA
+        if (!ctl.latched && wn) {
+          if (a.latch) ctl.latched = 1;
+          if (ctl.switch_it < 0) ctl.switch_it = t;
+        }
         const double wsr = xsum(XS_RATE);
         const double sv = xsum(XS_FV);
         int st = xfirst(XS_ST2);
         const double total_power = scale == 1.0 ? power : power * scale * scale;
         if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
-        double rel = INFINITY;
+        double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
         if (t > 1) {
           const double den = fabs(ctl.wsr_last);
           rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
@@ -980,19 +1060,21 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         ctl.iters = t;
         ctl.wsr = wsr;
         ctl.f_v = sv;
-        ctl.last_weighted = ctl.weighted_now;
+        ctl.weighted_now = wn;
+        ctl.last_weighted = wn;
         if (a.trace && crank == 0) {
           double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
           tr[AMMMSE_TRACE_T] = (double)t;
           tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
           tr[AMMMSE_TRACE_F_VALUE] = sv;
           tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
-          tr[AMMMSE_TRACE_STAGE] = (double)ctl.weighted_now;
+          tr[AMMMSE_TRACE_STAGE] = wn ? 1.0 : 0.0;
           tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
           tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
           tr[AMMMSE_TRACE_F_AFTER_V] = sv;
           tr[AMMMSE_TRACE_REL_CHANGE] = rel;
         }
+        // divergence detector (solvers.py:490-500)
         ctl.running_max = fmax(ctl.running_max, wsr);
         if (wsr < 0.5 * ctl.running_max)
           ctl.drop_streak += 1;
@@ -1003,16 +1085,25 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
           ctl.status = st;
           ctl.stop = 1;
         } else {
-          ctl.cur = oth;
-          if (ctl.weighted_now && rel <= a.eps2) {
+          ctl.cur = oth;  // shift (solvers.py:502)
+          if (wn && rel <= a.eps2) {  // stop test (:503-505)
             ctl.converged = 1;
             ctl.stop = 1;
           }
         }
+        ctl.wn_next = stage_flag();
       }
       __syncthreads();
-      pc.mark(8);
+      pc.mark(6);
       if (ctl.stop) break;
+      wn = ctl.wn_next != 0;
+      if (more && wn != wn_spec) {  // mis-speculated stage flag: redo K1(t+1) (same inputs)
+        k1_phase(cur, wn, true, bk, bk ^ 1);
+      } else if (more) {
+        k1_gather();
+      }
+      __syncthreads();
+      pc.mark(7);
     }
 
     // ---------------- exit: stationarity residual (solvers.py:400-412) ----------------
@@ -1027,7 +1118,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       __syncthreads();
       gram_partials(Gr[oth], Gi[oth], 0);
       cl.sync();
-      k1_phase(oth, weighted, false);
+      k1_phase(oth, weighted, false, 0, 0);
       int st = xfirst(XS_ST1);
       __syncthreads();
       if (st == 0) {
@@ -1081,7 +1172,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     // all remote reads of this realization's exchange buffers are complete
     // before any CTA starts the next realization (its first writes)
     cl.sync();
-    pc.mark(9);
+    pc.mark(8);
   }
   pc.flush();
   if (TC && L.tc) {

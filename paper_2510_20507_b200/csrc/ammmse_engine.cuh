@@ -302,6 +302,23 @@ __device__ __forceinline__ void vload(R (&dst)[W], const R* src) {
   }
 }
 
+template <typename R, int W>
+__device__ __forceinline__ void vstore(R* dst, const R (&src)[W]) {
+  using VT = typename V16<R>::T;
+  constexpr int n = V16<R>::n;
+  static_assert(W % n == 0, "vector width");
+#pragma unroll
+  for (int v = 0; v < W / n; ++v) {
+    VT x;
+    if constexpr (n == 4) {
+      x.x = src[4 * v]; x.y = src[4 * v + 1]; x.z = src[4 * v + 2]; x.w = src[4 * v + 3];
+    } else {
+      x.x = src[2 * v]; x.y = src[2 * v + 1];
+    }
+    reinterpret_cast<VT*>(dst)[v] = x;
+  }
+}
+
 template <typename R, int RY, int RX, int KU>
 __host__ __device__ inline bool cgemm_ok(int P, int Q, int KD, int lda, int ldb, int S, int threads) {
   constexpr int n = 16 / (int)sizeof(R);
@@ -318,11 +335,12 @@ __host__ __device__ inline int pick_split(int tiles, int threads, int KD, int KU
   return S;
 }
 
-template <typename R, int RY, int RX, int KU, bool CONJT, class Epi>
+// erow(p, q0, cr[RX], ci[RX]) receives one row run of RX consecutive outputs.
+template <typename R, int RY, int RX, int KU, bool CONJT, class ERow>
 __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R* __restrict__ Ar,
                                            const R* __restrict__ Ai, int lda,
                                            const R* __restrict__ Br, const R* __restrict__ Bi,
-                                           int ldb, Epi epi) {
+                                           int ldb, ERow erow) {
   // operands live in shared memory: let the compiler emit LDS (not generic LD)
   __builtin_assume(__isShared(Ar));
   __builtin_assume(__isShared(Ai));
@@ -395,28 +413,38 @@ __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R*
         ci[i][j] += __shfl_xor_sync(0xffffffffu, ci[i][j], o);
       }
   }
-  if (active) {  // lane s of the tile writes rows i = s, s+S, ...
+  if (active) {  // lane s of the tile writes rows i = s, s+S, ... (one RX run per row)
 #pragma unroll
     for (int i = 0; i < RY; ++i)
-      if (i % S == s)
-#pragma unroll
-        for (int j = 0; j < RX; ++j) epi(p0 + i, q0 + j, cr[i][j], ci[i][j]);
+      if (i % S == s) erow(p0 + i, q0, cr[i], ci[i]);
   }
 }
 
 // Dispatch: fast path when the shape allows, generic 2x2 path otherwise.
-template <typename R, int RY, int RX, bool CONJT, class Epi>
-__device__ __forceinline__ void cgemm_any(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
-                                          const R* Br, const R* Bi, int ldb, Epi epi) {
+// epi(p, q, re, im) per element; erow(p, q0, re[RX], im[RX]) per row run on
+// the fast path (vectorised epilogues: RX % (16 / sizeof(R)) == 0, output
+// row stride and base 16-byte aligned).
+template <typename R, int RY, int RX, bool CONJT, class Epi, class ERow>
+__device__ __forceinline__ void cgemm_any2(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
+                                           const R* Br, const R* Bi, int ldb, Epi epi, ERow erow) {
   constexpr int KU = 16 / (int)sizeof(R);
   const int tiles = (P % RY || Q % RX) ? 0 : (P / RY) * (Q / RX);
   const int S = tiles ? pick_split(tiles, blockDim.x, KD, CONJT ? 1 : KU) : 1;
   constexpr int KUe = CONJT ? 1 : KU;
   if (tiles && cgemm_ok<R, RY, RX, KUe>(P, Q, KD, lda, ldb, S, blockDim.x)) {
-    cgemm_fast<R, RY, RX, KUe, CONJT>(P, Q, KD, S, Ar, Ai, lda, Br, Bi, ldb, epi);
+    cgemm_fast<R, RY, RX, KUe, CONJT>(P, Q, KD, S, Ar, Ai, lda, Br, Bi, ldb, erow);
   } else {
     cgemm_smem<R, 2, 2, CONJT>(P, Q, KD, Ar, Ai, lda, Br, Bi, ldb, epi);
   }
+}
+template <typename R, int RY, int RX, bool CONJT, class Epi>
+__device__ __forceinline__ void cgemm_any(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
+                                          const R* Br, const R* Bi, int ldb, Epi epi) {
+  cgemm_any2<R, RY, RX, CONJT>(P, Q, KD, Ar, Ai, lda, Br, Bi, ldb, epi,
+                               [&](int p, int q0, const R(&cr)[RX], const R(&ci)[RX]) {
+#pragma unroll
+                                 for (int j = 0; j < RX; ++j) epi(p, q0 + j, cr[j], ci[j]);
+                               });
 }
 
 // Per-user Grams  gram[k] = sum_{j < ncols} X[kN+a][j] conj(X[kN+b][j])  (fp64),
@@ -462,6 +490,165 @@ __device__ __forceinline__ void user_grams(const R* __restrict__ Xr, const R* __
           if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
         }
     }
+  }
+}
+
+// Warp reduce-scatter of P (power of two <= 32) fp64 values: halving levels
+// (each lane keeps half of its values and ships the other half to its xor
+// partner), then a plain butterfly over the remaining lane bits.  P - 1 + (5 -
+// log2 P) shuffles instead of 5 P.  Returns value number lane >> (5 - log2 P)
+// summed over the warp, identical in every lane that holds it (fixed tree).
+template <int P, int H, int O>
+struct HalvingLevel {  // one halving level: keep H of 2H values, ship the others to lane ^ O
+  static __device__ __forceinline__ void run(double (&v)[P], int lane) {
+    const bool up = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const double send = up ? v[i] : v[H + i];
+      const double keep = up ? v[H + i] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    HalvingLevel<P, H / 2, O / 2>::run(v, lane);
+  }
+};
+template <int P, int O>
+struct HalvingLevel<P, 0, O> {
+  static __device__ __forceinline__ void run(double (&)[P], int) {}
+};
+template <int P>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[P], int lane) {
+  static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P power of two <= 32");
+  HalvingLevel<P, P / 2, 16>::run(v, lane);
+  constexpr int L = __builtin_ctz(P);
+#pragma unroll
+  for (int o = 16 >> L; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+
+// Packed Gram partial of user k over the columns j = lane, lane + 32, ... of
+// X: NN*(NN+1)/2 real parts of the lower triangle (row-major), then the
+// NN*(NN-1)/2 imaginary parts below the diagonal.
+template <typename R, int NN>
+__device__ __forceinline__ void gram_pack(const R* __restrict__ Xr, const R* __restrict__ Xi,
+                                          int ld, int k, int ncols, int lane, double* out) {
+  double sr[NN][NN], si[NN][NN];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
+  for (int j = lane; j < ncols; j += 32) {
+    double gr[NN], gi[NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      gr[a] = (double)Xr[(k * NN + a) * ld + j];
+      gi[a] = (double)Xi[(k * NN + a) * ld + j];
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
+        sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
+        if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
+      }
+  }
+  int n = 0;
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) out[n++] = sr[a][b];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < a; ++b) out[n++] = si[a][b];
+}
+
+// Store packed Gram value number `idx` (gram_pack order) into the Hermitian
+// N x N of user k.
+template <int NN>
+__device__ __forceinline__ void gram_store(int k, int idx, double val, cd* __restrict__ gram) {
+  constexpr int nre = NN * (NN + 1) / 2;
+  if (idx < nre) {
+    int a = 0;
+    while ((a + 1) * (a + 2) / 2 <= idx) ++a;
+    const int b = idx - a * (a + 1) / 2;
+    gram[(k * NN + a) * NN + b].r = val;
+    gram[(k * NN + b) * NN + a].r = val;
+    if (a == b) gram[(k * NN + a) * NN + a].i = 0.0;
+  } else {
+    const int m = idx - nre;
+    int a = 1;
+    while (a * (a + 1) / 2 <= m) ++a;
+    const int b = m - a * (a - 1) / 2;
+    gram[(k * NN + a) * NN + b].i = val;
+    gram[(k * NN + b) * NN + a].i = -val;
+  }
+}
+
+__host__ __device__ constexpr int pow2_at_least(int n) { return n <= 1 ? 1 : 2 * pow2_at_least((n + 1) / 2); }
+
+// Grams of user k over `ncols` columns of X0 (-> gram0) and, when X1 is not
+// null, of X1 (-> gram1): one warp, one packed reduce-scatter for both.
+template <typename R, int NN>
+__device__ __forceinline__ void gram_pair(int k, const R* X0r, const R* X0i, cd* gram0, const R* X1r,
+                                          const R* X1i, cd* gram1, int ld, int ncols, int lane) {
+  constexpr int V = NN * NN;
+  constexpr int P = pow2_at_least(2 * V);
+  double v[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) v[i] = 0.0;
+  gram_pack<R, NN>(X0r, X0i, ld, k, ncols, lane, v);
+  if (X1r) gram_pack<R, NN>(X1r, X1i, ld, k, ncols, lane, v + V);
+  const double tot = warp_reduce_scatter<P>(v, lane);
+  constexpr int L = __builtin_ctz(P);
+  const int idx = lane >> (5 - L);
+  if ((lane & ((1 << (5 - L)) - 1)) == 0) {
+    if (idx < V)
+      gram_store<NN>(k, idx, tot, gram0);
+    else if (idx < 2 * V && X1r)
+      gram_store<NN>(k, idx - V, tot, gram1);
+  }
+}
+
+// Gram of user k over `ncols` columns of X, computed by one warp (lanes over
+// columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
+template <typename R, int NN>
+__device__ __forceinline__ void gram_one(int k, const R* __restrict__ Xr, const R* __restrict__ Xi,
+                                         int ld, int ncols, int lane, cd* __restrict__ gram) {
+  double sr[NN][NN], si[NN][NN];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
+  for (int j = lane; j < ncols; j += 32) {
+    double gr[NN], gi[NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      gr[a] = (double)Xr[(k * NN + a) * ld + j];
+      gi[a] = (double)Xi[(k * NN + a) * ld + j];
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
+        sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
+        if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      sr[a][b] = warp_allsum(sr[a][b]);
+      if (b < a) si[a][b] = warp_allsum(si[a][b]);
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
+        if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
+      }
   }
 }
 
@@ -813,20 +1000,55 @@ struct Engine {
     const int ldg = L.ldg;
     AMMMSE_SHARED(gr);
     AMMMSE_SHARED(gi);
-    cgemm_any<R, 2, 4, false>(L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
-                               [&](int p, int q, R cr, R ci) {
-                                 const int o = p * ldg + q;
-                                 cr *= sc;  // G = H (c X) = c (H X): projection applied lazily
-                                 ci *= sc;
-                                 gr[o] = cr;
-                                 gi[o] = ci;
-                                 if (hr) {
-                                   AMMMSE_SHARED(hr);
-                                   AMMMSE_SHARED(hi);
-                                   hr[o] = cr + om * (cr - hr[o]);
-                                   hi[o] = ci + om * (ci - hi[o]);
-                                 }
-                               });
+    constexpr int RX = 4;
+    cgemm_any2<R, 2, RX, false>(
+        L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
+        [&](int p, int q, R cr, R ci) {
+          const int o = p * ldg + q;
+          cr *= sc;  // G = H (c X) = c (H X): projection applied lazily
+          ci *= sc;
+          gr[o] = cr;
+          gi[o] = ci;
+          if (hr) {  // ω = 0: plain copy (G_prev may be uninitialised shared memory)
+            AMMMSE_SHARED(hr);
+            AMMMSE_SHARED(hi);
+            hr[o] = om == R(0) ? cr : cr + om * (cr - hr[o]);
+            hi[o] = om == R(0) ? ci : ci + om * (ci - hi[o]);
+          }
+        },
+        [&](int p, int q0, const R(&cr)[RX], const R(&ci)[RX]) {  // 128-bit row runs
+          const int o = p * ldg + q0;
+          R c_r[RX], c_i[RX];
+#pragma unroll
+          for (int j = 0; j < RX; ++j) {
+            c_r[j] = cr[j] * sc;
+            c_i[j] = ci[j] * sc;
+          }
+          vstore<R, RX>(gr + o, c_r);
+          vstore<R, RX>(gi + o, c_i);
+          if (hr) {
+            AMMMSE_SHARED(hr);
+            AMMMSE_SHARED(hi);
+            R h_r[RX], h_i[RX];
+            if (om == R(0)) {  // plain copy (G_prev may be uninitialised shared memory)
+#pragma unroll
+              for (int j = 0; j < RX; ++j) {
+                h_r[j] = c_r[j];
+                h_i[j] = c_i[j];
+              }
+            } else {
+              vload<R, RX>(h_r, hr + o);
+              vload<R, RX>(h_i, hi + o);
+#pragma unroll
+              for (int j = 0; j < RX; ++j) {
+                h_r[j] = c_r[j] + om * (c_r[j] - h_r[j]);
+                h_i[j] = c_i[j] + om * (c_i[j] - h_i[j]);
+              }
+            }
+            vstore<R, RX>(hr + o, h_r);
+            vstore<R, RX>(hi + o, h_i);
+          }
+        });
   }
 
   // GEMM-A + projection input: X = V̂ − step · H^H Ŷ into V[dst] (unscaled).
@@ -848,20 +1070,54 @@ struct Engine {
     const int ldv = L.ldv;
     const R st = (R)step, om = (R)omega, sc = (R)sc_cur, so = (R)sc_old;
     double pw = 0.0;
-    cgemm_any<R, 4, 4, true>(L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
-                              [&](int p, int q, R gr, R gi) {
-                                const int o = p * ldv + q;
-                                R vr = sc * vcr[o], vi = sc * vci[o];
-                                if (extrap) {  // cur + ω (cur − prev)   (solvers.py:390)
-                                  vr = vr + om * (vr - so * xr[o]);
-                                  vi = vi + om * (vi - so * xi[o]);
-                                }
-                                const R x_r = vr - st * gr;
-                                const R x_i = vi - st * gi;
-                                xr[o] = x_r;
-                                xi[o] = x_i;
-                                pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
-                              });
+    constexpr int RX = 4;
+    cgemm_any2<R, 4, RX, true>(
+        L.M, L.KD, L.KN, Hr, Hi, L.ldh, Gr[ysrc], Gi[ysrc], L.ldg,
+        [&](int p, int q, R gr, R gi) {
+          const int o = p * ldv + q;
+          R vr = sc * vcr[o], vi = sc * vci[o];
+          if (extrap) {  // cur + ω (cur − prev)   (solvers.py:390)
+            vr = vr + om * (vr - so * xr[o]);
+            vi = vi + om * (vi - so * xi[o]);
+          }
+          const R x_r = vr - st * gr;
+          const R x_i = vi - st * gi;
+          xr[o] = x_r;
+          xi[o] = x_i;
+          pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
+        },
+        [&](int p, int q0, const R(&gr)[RX], const R(&gi)[RX]) {  // 128-bit row runs
+          const int o = p * ldv + q0;
+          R vr[RX], vi[RX];
+          vload<R, RX>(vr, vcr + o);
+          vload<R, RX>(vi, vci + o);
+          if (extrap) {
+            R pr[RX], pi[RX];
+            vload<R, RX>(pr, xr + o);
+            vload<R, RX>(pi, xi + o);
+#pragma unroll
+            for (int j = 0; j < RX; ++j) {
+              vr[j] = sc * vr[j];
+              vi[j] = sc * vi[j];
+              vr[j] = vr[j] + om * (vr[j] - so * pr[j]);
+              vi[j] = vi[j] + om * (vi[j] - so * pi[j]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < RX; ++j) {
+              vr[j] = sc * vr[j];
+              vi[j] = sc * vi[j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < RX; ++j) {
+            vr[j] = vr[j] - st * gr[j];
+            vi[j] = vi[j] - st * gi[j];
+            pw += (double)vr[j] * (double)vr[j] + (double)vi[j] * (double)vi[j];
+          }
+          vstore<R, RX>(xr + o, vr);
+          vstore<R, RX>(xi + o, vi);
+        });
     pw = warp_allsum(pw);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pw;
   }
@@ -985,6 +1241,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       __syncthreads();
     }
 
+    pc.mark(7);  // setup: load, bounds, G = H V0, K1(1)
     // ---------------- main loop (solvers.py:440-505), software-pipelined ----------------
     // Per iteration t: Ŷ(t) | GEMM-A + ‖X‖² | GEMM-B (+ Ĝ(t+1)) | Gram(G_new) and
     // Gram(Ĝ(t+1)) on all warps | warp 0: rates, reductions, state machine of t
@@ -1036,15 +1293,11 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       __syncthreads();
       pc.mark(3);
       const bool more = t < a.max_iters;
-      {  // Gram(G_new) -> gramb[1] and Gram(Ĝ(t+1)) -> gramb[0], all warps
+      {  // Gram(G_new) -> gramb[1] and Gram(Ĝ(t+1)) -> gramb[0], one warp per user
         const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-        const int ntask = more ? 2 * K : K;
-        for (int i = warp; i < ntask; i += nw) {
-          if (i < K)
-            e.gram_user(i, e.Gr[oth], e.Gi[oth], ldg, KD, lane, e.gramb[1]);
-          else
-            e.gram_user(i - K, e.Gr[cur], e.Gi[cur], ldg, KD, lane, e.gramb[0]);
-        }
+        for (int k = warp; k < K; k += nw)
+          gram_pair<R, NN>(k, e.Gr[oth], e.Gi[oth], e.gramb[1], more ? e.Gr[cur] : nullptr,
+                           e.Gi[cur], e.gramb[0], ldg, KD, lane);
       }
       // speculated stage flag of t+1: read before the barrier (thread 0 updates
       // ctl.latched in the next phase)
@@ -1193,6 +1446,7 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       }
     }
 
+    pc.mark(8);  // exit: stationarity residual
     // ---------------- write results ----------------
     {
       const int cur = ctl.cur;
