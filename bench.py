@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-phase-profile", action="store_true",
+                    help="skip the extra instrumented launch (bcgd_step share)")
     ap.add_argument("--cluster-size", type=int, default=0, help="engine knob (0 = automatic)")
     ap.add_argument("--h-placement", type=int, default=0, help="engine knob (0 = automatic)")
     ap.add_argument("--tensor-cores", type=int, default=0, help="engine knob (0 auto, 1 on, 2 off)")
@@ -351,6 +353,44 @@ def main():
                 f"realization-iterations per launch",
         "kernel": "ammmse_solve_kernel (1 launch per step)",
     }
+
+    # BCGD-step share of the kernel (GEMM-step fraction =
+    # F x realization-iterations / t_GEMM / peak): one extra, untimed solve with
+    # the engine's phase timers (thread-0 clock64 per phase), after the timed region.
+    if not args.no_phase_profile:
+        import ctypes
+
+        from paper_2510_20507_b200 import _native
+
+        os.environ["AMMMSE_PROFILE_PHASES"] = "1"
+        eng.solve(dH, ds2, dP, dA, dV0, out=res, stream=stream, **kw)
+        torch.cuda.synchronize()
+        del os.environ["AMMMSE_PROFILE_PHASES"]
+        sh = (ctypes.c_double * 16)()
+        f0, nb = ctypes.c_int(), ctypes.c_int()
+        n = _native.lib().ammmse_last_phase_profile(sh, 16, ctypes.byref(f0), ctypes.byref(nb))
+        if n > 0:
+            share = sum(sh[f0.value + i] for i in range(nb.value))
+            roofline["bcgd_step"] = {
+                "share_of_kernel": share, "frac": roofline["frac"] / share if share > 0 else None,
+                "achieved": roofline["achieved"] / share if share > 0 else None,
+                "phases": [round(sh[i], 4) for i in range(n)],
+                "note": "F x realization-iterations / time in the BCGD step phases (GEMM-A + "
+                        "step + projection, GEMM-B) / peak; phase shares from thread-0 clock64 "
+                        "timers of one extra untimed launch"}
+
+    # DRAM traffic of the same kernel from the committed ncu --set full capture
+    # (profiles/ncu_traffic.json, per realization), scaled to this launch, next
+    # to the algorithmic bytes (H and V0 read once, V_out written once).
+    tdb_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    tdb = json.load(open(tdb_path)) if os.path.exists(tdb_path) else {}
+    bpr = bytes_per_realization(w, itemsize)
+    roofline["algorithmic_bytes"] = int(B * (bpr["h2d"] + bpr["d2h"]))
+    if label in tdb:
+        ent = tdb[label]
+        roofline["traffic"] = int(ent["bytes_per_realization"] * B)
+        roofline["traffic_source"] = (f"{ent['source']}: ncu dram__bytes_read+write of "
+                                      f"{ent['realizations']} realizations, scaled to {B}")
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -169,6 +169,15 @@ int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* we
    this thread if any. */
 const char* ammmse_error_string(int code);
 
+/* Diagnostics (no reference counterpart).  When the environment variable
+   AMMMSE_PROFILE_PHASES=1 is set, ammmse_solve synchronises its stream and
+   records per-phase shares of the solve kernel's CTA-cycles (thread 0 clock64
+   deltas).  Copies up to n shares of the last profiled solve into `shares`
+   and returns the number of phases (0 if none); *bcgd_first / *bcgd_count
+   name the phases of the BCGD precoder step (GEMM-A + step + projection,
+   GEMM-B). */
+int ammmse_last_phase_profile(double* shares, int n, int* bcgd_first, int* bcgd_count);
+
 #ifdef __cplusplus
 }
 #endif

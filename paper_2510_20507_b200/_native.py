@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "ammmse_solve",
     "ammmse_bounds",
     "ammmse_error_string",
+    "ammmse_last_phase_profile",
 )
 
 
@@ -86,6 +87,10 @@ def lib() -> ctypes.CDLL:
             h = ctypes.CDLL(path)
         except OSError as exc:
             raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+        h.ammmse_last_phase_profile.restype = ctypes.c_int
+        h.ammmse_last_phase_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                                ctypes.POINTER(ctypes.c_int),
+                                                ctypes.POINTER(ctypes.c_int)]
         h.ammmse_abi_version.restype = ctypes.c_int
         h.ammmse_abi_version.argtypes = []
         h.ammmse_check_dims.restype = ctypes.c_int

@@ -19,6 +19,9 @@
 namespace {
 
 thread_local char g_err[256];
+// last AMMMSE_PROFILE_PHASES solve (diagnostics)
+static double g_phase_share[16];
+static int g_phase_n = 0;
 
 const ammmse::KernelEntry* lookup(const AmmmseDims* d) {
   if (d->N < 1 || d->N > 4 || d->d < 1 || d->d > 4) return nullptr;
@@ -381,12 +384,22 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     cudaStreamSynchronize(s);
     double tot = 0;
     for (int i = 0; i < 10; ++i) tot += (double)h[i];
+    for (int i = 0; i < 10; ++i) g_phase_share[i] = tot > 0 ? (double)h[i] / tot : 0.0;
+    g_phase_n = 10;  // both engines: p2 = GEMM-A + step + projection, p3 = GEMM-B (+ Grams)
     fprintf(stderr, "[ammmse phases] engine=%s C=%d hres=%d:", plan.cluster ? "cluster" : "single",
             plan.cluster, plan.hres);
     for (int i = 0; i < 10; ++i) fprintf(stderr, " p%d=%.1f%%", i, tot > 0 ? 100.0 * h[i] / tot : 0.0);
     fprintf(stderr, " (total %.3g CTA-cycles)\n", tot);
   }
   return AMMMSE_OK;
+}
+
+int ammmse_last_phase_profile(double* shares, int n, int* bcgd_first, int* bcgd_count) {
+  if (bcgd_first) *bcgd_first = 2;
+  if (bcgd_count) *bcgd_count = 2;
+  if (shares)
+    for (int i = 0; i < n && i < g_phase_n; ++i) shares[i] = g_phase_share[i];
+  return g_phase_n;
 }
 
 int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* weights,

@@ -336,11 +336,18 @@ __host__ __device__ inline int pick_split(int tiles, int threads, int KD, int KU
 }
 
 // erow(p, q0, cr[RX], ci[RX]) receives one row run of RX consecutive outputs.
-template <typename R, int RY, int RX, int KU, bool CONJT, class ERow>
+struct NoTile {
+  template <class... T>
+  __device__ __forceinline__ void operator()(T&&...) const {}
+};
+
+// etile(active, s, p0, q0, cr, ci) is then called by EVERY lane (inactive
+// lanes too, so it may use full-warp shuffles) with the complete RY x RX tile.
+template <typename R, int RY, int RX, int KU, bool CONJT, class ERow, class ETile = NoTile>
 __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R* __restrict__ Ar,
                                            const R* __restrict__ Ai, int lda,
                                            const R* __restrict__ Br, const R* __restrict__ Bi,
-                                           int ldb, ERow erow) {
+                                           int ldb, ERow erow, ETile etile = ETile()) {
   // operands live in shared memory: let the compiler emit LDS (not generic LD)
   __builtin_assume(__isShared(Ar));
   __builtin_assume(__isShared(Ai));
@@ -418,6 +425,7 @@ __device__ __forceinline__ void cgemm_fast(int P, int Q, int KD, int S, const R*
     for (int i = 0; i < RY; ++i)
       if (i % S == s) erow(p0 + i, q0, cr[i], ci[i]);
   }
+  etile(active, s, p0, q0, cr, ci);
 }
 
 // Dispatch: fast path when the shape allows, generic 2x2 path otherwise.
@@ -437,6 +445,23 @@ __device__ __forceinline__ void cgemm_any2(int P, int Q, int KD, const R* Ar, co
     cgemm_smem<R, 2, 2, CONJT>(P, Q, KD, Ar, Ai, lda, Br, Bi, ldb, epi);
   }
 }
+// Same, plus a tile hook on the fast path; returns true when the fast path ran.
+template <typename R, int RY, int RX, bool CONJT, class Epi, class ERow, class ETile>
+__device__ __forceinline__ bool cgemm_any3(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
+                                           const R* Br, const R* Bi, int ldb, Epi epi, ERow erow,
+                                           ETile etile) {
+  constexpr int KU = 16 / (int)sizeof(R);
+  const int tiles = (P % RY || Q % RX) ? 0 : (P / RY) * (Q / RX);
+  const int S = tiles ? pick_split(tiles, blockDim.x, KD, CONJT ? 1 : KU) : 1;
+  constexpr int KUe = CONJT ? 1 : KU;
+  if (tiles && cgemm_ok<R, RY, RX, KUe>(P, Q, KD, lda, ldb, S, blockDim.x)) {
+    cgemm_fast<R, RY, RX, KUe, CONJT>(P, Q, KD, S, Ar, Ai, lda, Br, Bi, ldb, erow, etile);
+    return true;
+  }
+  cgemm_smem<R, 2, 2, CONJT>(P, Q, KD, Ar, Ai, lda, Br, Bi, ldb, epi);
+  return false;
+}
+
 template <typename R, int RY, int RX, bool CONJT, class Epi>
 __device__ __forceinline__ void cgemm_any(int P, int Q, int KD, const R* Ar, const R* Ai, int lda,
                                           const R* Br, const R* Bi, int ldb, Epi epi) {
@@ -522,6 +547,18 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[P], int lane) 
   constexpr int L = __builtin_ctz(P);
 #pragma unroll
   for (int o = 16 >> L; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+
+// Reduce-scatter of P values within aligned groups of G lanes (P <= G, both
+// powers of two): halving levels at offsets G/2 ... G/P, then a butterfly over
+// the remaining lower offsets.  Lane l returns value number (l % G) / (G / P).
+template <int P, int G>
+__device__ __forceinline__ double group_reduce_scatter(double (&v)[P], int lane) {
+  static_assert(P >= 1 && P <= G && G <= 32 && (P & (P - 1)) == 0 && (G & (G - 1)) == 0, "");
+  HalvingLevel<P, P / 2, G / 2>::run(v, lane);
+#pragma unroll
+  for (int o = G / P / 2; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
   return v[0];
 }
 
@@ -990,8 +1027,15 @@ struct Engine {
   // GEMM-B: G[dst] = H · V[src].  With ghat >= 0 the epilogue also writes the
   // next iteration's extrapolated Ĝ = G + ω (G − G_prev) (solvers.py:380-390,
   // by linearity) over G[ghat], which holds G_prev = the current G.
-  __device__ void gemm_hv(int src, int dst, int ghat = -1, double omega = 0.0,
-                          double vscale = 1.0) {
+  //
+  // fuse_gram: also form the fp64 Grams of G[dst] (-> gramb[1]) and of Ĝ (->
+  // gramb[0]) in the tile epilogue, when the tile layout allows (N = 2 = tile
+  // rows, split S <= 2, a user's QT >= 8 column tiles in consecutive lanes):
+  // each lane packs the partial Grams of its 2 x 4 tile, and a group
+  // reduce-scatter over the user's QT lanes finishes them (no separate Gram
+  // pass, one block barrier fewer).  Returns whether the Grams were formed.
+  __device__ bool gemm_hv(int src, int dst, int ghat = -1, double omega = 0.0,
+                          double vscale = 1.0, bool fuse_gram = false) {
     R* gr = Gr[dst];
     R* gi = Gi[dst];
     R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
@@ -1001,7 +1045,80 @@ struct Engine {
     AMMMSE_SHARED(gr);
     AMMMSE_SHARED(gi);
     constexpr int RX = 4;
-    cgemm_any2<R, 2, RX, false>(
+    bool fuse = false;
+    int QT = 0;
+    if constexpr (NN == 2) {
+      if (fuse_gram && L.KD % RX == 0) {
+        constexpr int KU = 16 / (int)sizeof(R);
+        QT = L.KD / RX;
+        const int tiles = (L.KN / 2) * QT;
+        const int S = pick_split(tiles, blockDim.x, L.M, KU);
+        fuse = S <= 2 && QT >= 8 && (QT & (QT - 1)) == 0 && QT <= 32 / S &&
+               cgemm_ok<R, 2, RX, KU>(L.KN, L.KD, L.M, L.ldh, L.ldv, S, blockDim.x);
+      }
+    }
+    cd* gnew = gramb[1];
+    cd* ghatg = gramb[0];
+    auto etile = [&](bool active, int s, int p0, int q0, const R(&cr)[2][RX],
+                     const R(&ci)[2][RX]) {
+      if constexpr (NN == 2) {
+        if (!fuse) return;
+        const int lane = threadIdx.x & 31;
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0.0;
+        __syncwarp();  // Ĝ rows stored by the tile's other split lane are visible
+        if (active) {
+#pragma unroll
+          for (int j = 0; j < RX; ++j) {  // gram_pack order: (0,0) (1,0) (1,1) re, (1,0) im
+            const double g0r = (double)(cr[0][j] * sc), g0i = (double)(ci[0][j] * sc);
+            const double g1r = (double)(cr[1][j] * sc), g1i = (double)(ci[1][j] * sc);
+            v[0] = fma(g0r, g0r, fma(g0i, g0i, v[0]));
+            v[1] = fma(g1r, g0r, fma(g1i, g0i, v[1]));
+            v[2] = fma(g1r, g1r, fma(g1i, g1i, v[2]));
+            v[3] = fma(g1i, g0r, fma(-g1r, g0i, v[3]));
+          }
+          if (hr) {
+            AMMMSE_SHARED(hr);
+            AMMMSE_SHARED(hi);
+            R h0r[RX], h0i[RX], h1r[RX], h1i[RX];
+            vload<R, RX>(h0r, hr + p0 * ldg + q0);
+            vload<R, RX>(h0i, hi + p0 * ldg + q0);
+            vload<R, RX>(h1r, hr + (p0 + 1) * ldg + q0);
+            vload<R, RX>(h1i, hi + (p0 + 1) * ldg + q0);
+#pragma unroll
+            for (int j = 0; j < RX; ++j) {
+              const double g0r = h0r[j], g0i = h0i[j], g1r = h1r[j], g1i = h1i[j];
+              v[4] = fma(g0r, g0r, fma(g0i, g0i, v[4]));
+              v[5] = fma(g1r, g0r, fma(g1i, g0i, v[5]));
+              v[6] = fma(g1r, g1r, fma(g1i, g1i, v[6]));
+              v[7] = fma(g1i, g0r, fma(-g1r, g0i, v[7]));
+            }
+          }
+        }
+        double tot;
+        int idx;
+        if (QT == 8) {
+          tot = group_reduce_scatter<8, 8>(v, lane);
+          idx = lane & 7;
+        } else if (QT == 16) {
+          tot = group_reduce_scatter<8, 16>(v, lane);
+          idx = (lane & 15) >> 1;
+        } else {
+          tot = group_reduce_scatter<8, 32>(v, lane);
+          idx = lane >> 2;
+        }
+        const int sub = QT / 8;  // lanes per value
+        if (active && s == 0 && (lane % sub) == 0) {
+          const int k = p0 / 2;
+          if (idx < 4)
+            gram_store<2>(k, idx, tot, gnew);
+          else if (hr)
+            gram_store<2>(k, idx - 4, tot, ghatg);
+        }
+      }
+    };
+    const bool fast = cgemm_any3<R, 2, RX, false>(
         L.KN, L.KD, L.M, Hr, Hi, L.ldh, Vr[src], Vi[src], L.ldv,
         [&](int p, int q, R cr, R ci) {
           const int o = p * ldg + q;
@@ -1048,7 +1165,9 @@ struct Engine {
             vstore<R, RX>(hr + o, h_r);
             vstore<R, RX>(hi + o, h_i);
           }
-        });
+        },
+        etile);
+    return fast && fuse;
   }
 
   // GEMM-A + projection input: X = V̂ − step · H^H Ŷ into V[dst] (unscaled).
@@ -1289,20 +1408,22 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1)
       double scale = 1.0;
       if (!(power <= pmax)) scale = sqrt(pmax / power);
       // G_new = H V_new = scale (H X) over Ŷ; next Ĝ over G_cur (which becomes G_old)
-      e.gemm_hv(oth, oth, cur, ctl.omega, scale);
+      // (Grams of G_new -> gramb[1] and Ĝ(t+1) -> gramb[0] in its tile epilogue
+      // when the layout allows)
+      const bool fused = e.gemm_hv(oth, oth, cur, ctl.omega, scale, true);
+      // speculated stage flag of t+1: read before the barrier (thread 0 updates
+      // ctl.latched in the next phase)
+      const bool wn_spec = ctl.latched || wn;
+      const bool more = t < a.max_iters;
       __syncthreads();
       pc.mark(3);
-      const bool more = t < a.max_iters;
-      {  // Gram(G_new) -> gramb[1] and Gram(Ĝ(t+1)) -> gramb[0], one warp per user
+      if (!fused) {  // Gram(G_new) -> gramb[1] and Gram(Ĝ(t+1)) -> gramb[0], one warp per user
         const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
         for (int k = warp; k < K; k += nw)
           gram_pair<R, NN>(k, e.Gr[oth], e.Gi[oth], e.gramb[1], more ? e.Gr[cur] : nullptr,
                            e.Gi[cur], e.gramb[0], ldg, KD, lane);
+        __syncthreads();
       }
-      // speculated stage flag of t+1: read before the barrier (thread 0 updates
-      // ctl.latched in the next phase)
-      const bool wn_spec = ctl.latched || wn;
-      __syncthreads();
       pc.mark(4);
       if (tid < 32) {  // warp 0: rates (lanes = users), reductions, state machine
         const int lane = tid;
