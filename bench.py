@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
+                    help="slices of the pipelined host-buffer solve in the e2e measurement")
     ap.add_argument("--no-phase-profile", action="store_true",
                     help="skip the extra instrumented launch (bcgd_step share)")
     ap.add_argument("--cluster-size", type=int, default=0, help="engine knob (0 = automatic)")
@@ -295,11 +297,10 @@ def main():
         dbufs = [torch.empty_like(x, device=dev) for x in (hH, hs2, hP, hA, hV0)]
 
         def e2e_step():
-            for d_, h_ in zip(dbufs, (hH, hs2, hP, hA, hV0)):
-                d_.copy_(h_, non_blocking=True)
-            r = eng.solve(*dbufs, out=res, stream=stream, **kw)
-            for k, h_ in hout.items():
-                h_.copy_(getattr(r, k), non_blocking=True)
+            # public API, host buffers: H2D of slice i+1 and D2H of slice i-1
+            # overlap the solve of slice i (AmmmseEngine.solve_host)
+            r = eng.solve_host((hH, hs2, hP, hA, hV0), hout, dbufs, res, stream=stream,
+                               chunks=args.e2e_chunks, **kw)
             if world > 1:
                 local_res = torch.stack([r.wsr_bits, r.iterations.to(torch.float64)], dim=1)
                 dist.all_gather_into_tensor(gather_buf.view(world * B, 2), local_res)

@@ -277,7 +277,7 @@ class AmmmseEngine:
     def solve(self, channels, noise_power, p_max, weights, init_precoders, *, gamma, omega,
               eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
               out: BatchResult | None = None, stream=None, cluster_size: int = 0,
-              h_placement: int = 0, tensor_cores: int = 0) -> BatchResult:
+              h_placement: int = 0, tensor_cores: int = 0, workspace=None) -> BatchResult:
         torch = _torch()
         dims = self.dims(channels, init_precoders)
         self.check(dims)
@@ -330,7 +330,10 @@ class AmmmseEngine:
         if ws_bytes == 0:
             raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
                               f"h_placement={h_placement}, tensor_cores={tensor_cores})")
-        ws = self._workspace(ws_bytes)
+        if workspace is not None and workspace.numel() >= ws_bytes:
+            ws = workspace  # caller-owned (concurrent solves on several streams)
+        else:
+            ws = self._workspace(ws_bytes)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
         rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
@@ -341,6 +344,62 @@ class AmmmseEngine:
             raise NativeLibraryError(f"ammmse_solve failed: {_native.error_string(rc)}")
         out.omega = omega if o_arr is None else o_arr
         return out
+
+    _RESULT_FIELDS = ("final_precoders", "wsr_bits", "iterations", "converged",
+                      "stationarity_residual", "switch_iteration", "status")
+
+    def solve_host(self, host_inputs, host_out, dev_inputs, dev_out: BatchResult, *, gamma, omega,
+                   chunks: int = 4, stream=None, **kw) -> BatchResult:
+        """End-to-end solve of HOST (pinned) arrays, pipelined in `chunks`
+        slices over two CUDA streams: the host->device copy of slice i+1 and the
+        device->host copy of slice i-1 overlap the solve of slice i, and the
+        next slice's kernel fills the SMs the previous one's tail leaves idle.
+
+        host_inputs / dev_inputs: (channels, noise_power, p_max, weights,
+        init_precoders); host_out: dict of pinned tensors keyed by the
+        BatchResult fields in _RESULT_FIELDS; dev_out: device BatchResult;
+        gamma / omega: scalars or (B,) device tensors.  Stream-ordered on
+        `stream` (default: the current stream); returns dev_out."""
+        torch = _torch()
+        dev = self.device
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        B = int(host_inputs[0].shape[0])
+        chunks = max(1, min(int(chunks), B))
+        if not hasattr(self, "_side"):
+            self._side = [torch.cuda.Stream(dev) for _ in range(2)]
+            self._side_ws = [None, None]
+        start = torch.cuda.Event()
+        start.record(stream)
+        bounds = [B * c // chunks for c in range(chunks + 1)]
+        for c in range(chunks):
+            a, b = bounds[c], bounds[c + 1]
+            if b <= a:
+                continue
+            s = self._side[c % 2]
+            s.wait_event(start)
+            with torch.cuda.stream(s):
+                for d_, h_ in zip(dev_inputs, host_inputs):
+                    d_[a:b].copy_(h_[a:b], non_blocking=True)
+                sub = BatchResult(*(getattr(dev_out, f)[a:b] for f in self._RESULT_FIELDS),
+                                  gamma_used=dev_out.gamma_used[a:b])
+                g = gamma[a:b] if torch.is_tensor(gamma) else gamma
+                o = omega[a:b] if torch.is_tensor(omega) else omega
+                dims = self.dims(dev_inputs[0][a:b], dev_inputs[4][a:b])
+                opts_kw = {k: kw[k] for k in ("cluster_size", "h_placement", "tensor_cores") if k in kw}
+                need = int(self.lib.ammmse_workspace_size_opts(dims, _native.AmmmseOptions(
+                    max_iters=int(kw.get("max_iters", 1000)), **opts_kw)))
+                wsb = self._side_ws[c % 2]
+                if wsb is None or wsb.numel() < need:
+                    wsb = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+                    self._side_ws[c % 2] = wsb
+                self.solve(*(x[a:b] for x in dev_inputs), gamma=g, omega=o, out=sub, stream=s,
+                           workspace=wsb, **kw)
+                for f, h_ in host_out.items():
+                    h_[a:b].copy_(getattr(dev_out, f)[a:b], non_blocking=True)
+        for s in self._side:
+            stream.wait_stream(s)
+        return dev_out
 
     def bounds(self, channels, weights, p_max, noise_power, stream=None):
         """Batched compute_bounds (ref objective.py:216-240): (B, 5) float64

@@ -234,3 +234,30 @@ def test_cluster_tensor_core_gemms_complex64(cuda, M, K, N, d, csize):
     # per-iteration WSR trajectories of the two GEMM engines agree closely
     n = min(tc.iterations.min(), ff.iterations.min())
     np.testing.assert_allclose(tc.trace[:, :n, 1], ff.trace[:, :n, 1], rtol=1e-5)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_pipelined_host_solve_matches_device_solve(cuda, chunks):
+    """AmmmseEngine.solve_host (host buffers, slices pipelined over two streams)
+    gives bit-identical results to one device solve of the whole batch."""
+    import torch
+
+    from paper_2510_20507_b200.solvers import AmmmseEngine
+
+    b = build_batch(64, 2, 16, 2, 40, p_max=100.0, weights="uniform", dtype=np.complex64)
+    eng = AmmmseEngine(cuda)
+    kw = dict(eps1=0.1, eps2=1e-5, max_iters=120)
+    host = tuple(torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in
+                 (b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders))
+    dev = tuple(x.to(cuda) for x in host)
+    ref = eng.solve(*dev, gamma=0.004, omega=0.8, **kw)
+    torch.cuda.synchronize()
+    ref = ref.to_host()
+    dbufs = [torch.empty_like(x, device=cuda) for x in host]
+    out = eng.solve(*dev, gamma=0.004, omega=0.8, **kw)  # device result buffers
+    hout = {f: torch.empty(tuple(getattr(out, f).shape), dtype=getattr(out, f).dtype).pin_memory()
+            for f in AmmmseEngine._RESULT_FIELDS}
+    eng.solve_host(host, hout, dbufs, out, gamma=0.004, omega=0.8, chunks=chunks, **kw)
+    torch.cuda.synchronize()
+    for f in AmmmseEngine._RESULT_FIELDS:
+        np.testing.assert_array_equal(hout[f].numpy(), getattr(ref, f), err_msg=f)
