@@ -198,7 +198,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4,
+    ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="slices of the pipelined host-buffer solve in the e2e measurement")
     ap.add_argument("--no-phase-profile", action="store_true",
                     help="skip the extra instrumented launch (bcgd_step share)")
