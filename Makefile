@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
 SRC_DIR := paper_2510_20507_b200/csrc
 OBJ_DIR := build/obj
-SRCS := $(SRC_DIR)/ammmse_capi.cu $(wildcard $(SRC_DIR)/inst/*.cu)
+SRCS := $(SRC_DIR)/ammmse_capi.cu $(SRC_DIR)/ammmse_gen.cu $(wildcard $(SRC_DIR)/inst/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS := include/ammmse.h $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/entries.h
 LIB := paper_2510_20507_b200/libammmse.so

@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--device-inputs", action="store_true",
+                    help="generate the (i.i.d.) workload on the device at its full batch size")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="slices of the pipelined host-buffer solve in the e2e measurement")
     ap.add_argument("--no-phase-profile", action="store_true",
@@ -230,17 +232,44 @@ def main():
     blocks, label = bench_workload(args.config)
     w = blocks[0]
     per_block = args.per_block or w.B
-    batch = build_inputs(blocks, per_block, seed0=rank * per_block, workers=args.gen_workers)
-    B = batch.B
-    itemsize = np.dtype(w.dtype).itemsize // 2
     eng = AmmmseEngine(dev)
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    itemsize = np.dtype(w.dtype).itemsize // 2
+    if args.device_inputs:
+        # i.i.d. workloads at their full BASELINE batch, generated on the device
+        # (ammmse_generate_iid; distributionally, not bit-, identical to the host
+        # generators); the CPU baseline still runs on a host-generated sample
+        if any(b.channel != "iid" for b in blocks):
+            raise SystemExit("--device-inputs supports the i.i.d. workloads only")
+        parts = [eng.generate_iid(per_block, b.K, b.N, b.M, b.d, seed0=rank * per_block,
+                                  p_max=b.p_max, weights=b.weights,
+                                  dtype=np.dtype(b.dtype).name) for b in blocks]
+        dH = torch.cat([p[0] for p in parts])
+        dV0 = torch.cat([p[1] for p in parts])
+        dA = torch.cat([p[2] for p in parts])
+        B = dH.shape[0]
+        ds2 = torch.ones(B, dtype=torch.float64, device=dev)
+        dP = torch.cat([torch.full((per_block,), b.p_max, dtype=torch.float64, device=dev)
+                        for b in blocks])
+        g_arr = torch.cat([torch.full((per_block,), b.gamma, dtype=torch.float64, device=dev)
+                           for b in blocks])
+        o_arr = torch.cat([torch.full((per_block,), b.omega, dtype=torch.float64, device=dev)
+                           for b in blocks])
+        del parts
+        cpu_pb = min(per_block, 256)
+        batch = build_inputs(blocks, cpu_pb, seed0=0, workers=args.gen_workers)
+        args.no_e2e = True  # inputs are created on the device: no host-buffer e2e number
+    else:
+        cpu_pb = per_block
+        batch = build_inputs(blocks, per_block, seed0=rank * per_block, workers=args.gen_workers)
+        B = batch.B
+        dH, ds2, dP, dA, dV0 = (to(batch.channels), to(batch.noise_power), to(batch.p_max),
+                                to(batch.weights), to(batch.init_precoders))
+        g_arr, o_arr = to(batch.gamma), to(batch.omega)
     # per-realization (gamma, omega): each SNR block carries its own step
-    kw = dict(gamma=to(batch.gamma), omega=to(batch.omega), eps1=w.eps1, eps2=w.eps2,
+    kw = dict(gamma=g_arr, omega=o_arr, eps1=w.eps1, eps2=w.eps2,
               max_iters=w.max_iters, cluster_size=args.cluster_size, h_placement=args.h_placement,
               tensor_cores=args.tensor_cores)
-    dH, ds2, dP, dA, dV0 = (to(batch.channels), to(batch.noise_power), to(batch.p_max),
-                            to(batch.weights), to(batch.init_precoders))
     stream = torch.cuda.current_stream(dev)
 
     gather_buf = torch.empty((world, B, 2), dtype=torch.float64, device=dev) if world > 1 else None
@@ -398,7 +427,7 @@ def main():
         from oracle.cpu_baseline import CpuPool
 
         pool = CpuPool()
-        r = cpu_time(blocks, batch, per_block, args.cpu_seconds, pool)
+        r = cpu_time(blocks, batch, cpu_pb, args.cpu_seconds, pool)
         pool.close()
         cpu = {"value": r["value"], "unit": UNIT, "cores": pool.workers, "kind": "port",
                "sample": f"{r['n']} realizations (round-robin over the SNR blocks, "
@@ -411,15 +440,16 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "c64 (fp32 GEMM, fp64 Gram/log-det/WSR)" if w.dtype == np.complex64 else "c128",
-        "data": "synthetic (seeded Philox inputs, SURVEY.md §8(d))",
+        "data": ("synthetic, generated on the device (Philox4x32-10 CN(0,1), ammmse_generate_iid)"
+                 if args.device_inputs else "synthetic (seeded Philox inputs, SURVEY.md §8(d))"),
         "config": {"workload": label, "M": w.M, "K": w.K, "N": w.N, "d": w.d,
                    "realizations_per_gpu_step": B, "snr_blocks": len(blocks),
                    "max_iters": w.max_iters, "eps2": w.eps2, "gamma": [b.gamma for b in blocks],
                    "omega": w.omega,
                    "mean_iterations": iters_total / B, "failed_realizations": n_bad,
                    "parallelism": f"dp{world} (realizations sharded, no data-path collective)",
-                   "l2": f"inputs larger than L2: {batch.channels.nbytes / 2**20:.0f} MiB of channels "
-                         f"read once per step"},
+                   "l2": f"inputs larger than L2: {dH.numel() * dH.element_size() / 2**20:.0f} MiB "
+                         f"of channels read once per step"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -169,6 +169,18 @@ int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* we
    this thread if any. */
 const char* ammmse_error_string(int code);
 
+/* On-device synthetic inputs: for realization r of
+   the batch, H (B, K, N, M) and V0 (B, K, M, d) i.i.d. CN(0,1) drawn from
+   Philox4x32-10 keyed by (seed0 + r, stream tag), V0 scaled onto the power
+   ball ||V0||^2 <= p_max (generate_channels model.py:197-207,
+   init_precoders model.py:225-235, project_sum_power solvers.py:257-263);
+   weights (B, K), optional: Uniform[0.5, 1.5) if uniform_weights else 1.
+   Distributionally (not bit-) identical to the reference's numpy streams.
+   Device pointers, stream-ordered. */
+int ammmse_generate_iid(const AmmmseDims* dims, unsigned long long seed0, double p_max,
+                        int uniform_weights, void* channels, void* init_precoders,
+                        double* weights, void* stream);
+
 /* Diagnostics (no reference counterpart).  When the environment variable
    AMMMSE_PROFILE_PHASES=1 is set, ammmse_solve synchronises its stream and
    records per-phase shares of the solve kernel's CTA-cycles (thread 0 clock64

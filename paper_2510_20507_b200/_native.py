@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "ammmse_bounds",
     "ammmse_error_string",
     "ammmse_last_phase_profile",
+    "ammmse_generate_iid",
 )
 
 
@@ -87,6 +88,10 @@ def lib() -> ctypes.CDLL:
             h = ctypes.CDLL(path)
         except OSError as exc:
             raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+        h.ammmse_generate_iid.restype = ctypes.c_int
+        h.ammmse_generate_iid.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.c_ulonglong,
+                                          ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         h.ammmse_last_phase_profile.restype = ctypes.c_int
         h.ammmse_last_phase_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                                                 ctypes.POINTER(ctypes.c_int),

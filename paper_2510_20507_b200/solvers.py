@@ -345,6 +345,35 @@ class AmmmseEngine:
         out.omega = omega if o_arr is None else o_arr
         return out
 
+    def generate_iid(self, B: int, K: int, N: int, M: int, d: int, *, seed0: int = 0,
+                     p_max: float = 10.0, weights: str = "uniform", dtype="complex64",
+                     stream=None):
+        """On-device synthetic batch (ammmse_generate_iid): channels (B, K, N, M)
+        and projected init_precoders (B, K, M, d) i.i.d. CN(0,1) from a Philox
+        stream keyed by seed0 + r, weights (B, K) Uniform[0.5, 1.5) or ones.
+        Distributionally identical to generate_channels / init_precoders,
+        not bit-identical (the host generators stay the bit-exact path)."""
+        torch = _torch()
+        ct = torch.complex64 if str(dtype).endswith("64") else torch.complex128
+        dev = self.device
+        H = torch.empty((B, K, N, M), dtype=ct, device=dev)
+        V0 = torch.empty((B, K, M, d), dtype=ct, device=dev)
+        A = torch.empty((B, K), dtype=torch.float64, device=dev)
+        if weights not in ("uniform", "ones"):
+            raise ConfigError("weights must be 'uniform' or 'ones'")
+        if not (p_max > 0 and math.isfinite(p_max)):
+            raise ConfigError("p_max must be a positive real")
+        dims = _native.AmmmseDims(B, M, N, K, d,
+                                  _native.COMPLEX64 if ct == torch.complex64 else _native.COMPLEX128)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        rc = self.lib.ammmse_generate_iid(dims, int(seed0), float(p_max),
+                                          1 if weights == "uniform" else 0, H.data_ptr(),
+                                          V0.data_ptr(), A.data_ptr(), ctypes_stream(stream))
+        if rc != 0:
+            raise NativeLibraryError(f"ammmse_generate_iid failed: {_native.error_string(rc)}")
+        return H, V0, A
+
     _RESULT_FIELDS = ("final_precoders", "wsr_bits", "iterations", "converged",
                       "stationarity_residual", "switch_iteration", "status")
 
