@@ -68,13 +68,33 @@ __device__ __forceinline__ bool chol_lower(cd (&A)[n][n]) {
   return true;
 }
 
-// ln det of the matrix whose Cholesky factor is L (linalg.py:27-30)
+// ln det of the matrix whose Cholesky factor is L (linalg.py:27-30): one log
+// of the product of the pivots (the per-user algebra is latency bound and an
+// fp64 log is a long dependent routine), the sum of logs only when the
+// product leaves the normal range.
 template <int n>
 __device__ __forceinline__ double chol_lndet(const cd (&L)[n][n]) {
+  double p = 1.0;
+#pragma unroll
+  for (int j = 0; j < n; ++j) p *= L[j][j].r * L[j][j].r;
+  if (p >= 2.2250738585072014e-308 && p <= 1.7976931348623157e308) return log(p);
   double s = 0.0;
 #pragma unroll
   for (int j = 0; j < n; ++j) s += log(L[j][j].r);
   return 2.0 * s;
+}
+
+// ln det(A) - ln det(C) from their Cholesky factors with a single log
+template <int n>
+__device__ __forceinline__ double chol_lndet_diff(const cd (&LA)[n][n], const cd (&LC)[n][n]) {
+  double q = 1.0;
+#pragma unroll
+  for (int j = 0; j < n; ++j) {
+    const double r = LA[j][j].r / LC[j][j].r;
+    q *= r * r;
+  }
+  if (q >= 2.2250738585072014e-308 && q <= 1.7976931348623157e308) return log(q);
+  return chol_lndet<n>(LA) - chol_lndet<n>(LC);
 }
 
 // Solve (L L^H) X = B in place, B is n x m (scipy cho_solve).

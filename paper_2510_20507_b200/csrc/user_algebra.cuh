@@ -393,7 +393,7 @@ __device__ __forceinline__ void wsr_math(const cd (&Tg)[NN][NN], const cd (&Gkk)
   status = 0;
   rate = 0.0;
   if (chol_lower<NN>(A) && chol_lower<NN>(Cv)) {
-    double r = chol_lndet<NN>(A) - chol_lndet<NN>(Cv);
+    double r = chol_lndet_diff<NN>(A, Cv);
     rate = ak * (r > 0.0 ? r : 0.0);
   } else {
     status = AMMMSE_STATUS_NONFINITE;
