@@ -236,14 +236,13 @@ def main():
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     itemsize = np.dtype(w.dtype).itemsize // 2
     if args.device_inputs:
-        # i.i.d. workloads at their full BASELINE batch, generated on the device
-        # (ammmse_generate_iid; distributionally, not bit-, identical to the host
-        # generators); the CPU baseline still runs on a host-generated sample
-        if any(b.channel != "iid" for b in blocks):
-            raise SystemExit("--device-inputs supports the i.i.d. workloads only")
-        parts = [eng.generate_iid(per_block, b.K, b.N, b.M, b.d, seed0=rank * per_block,
-                                  p_max=b.p_max, weights=b.weights,
-                                  dtype=np.dtype(b.dtype).name) for b in blocks]
+        # the workload at its full BASELINE batch, generated on the device
+        # (ammmse_generate_iid / generate_kronecker; distributionally, not bit-,
+        # identical to the host generators); the CPU baseline still runs on a
+        # host-generated sample
+        gen = lambda b: (eng.generate_iid if b.channel == "iid" else eng.generate_kronecker)
+        parts = [gen(b)(per_block, b.K, b.N, b.M, b.d, seed0=rank * per_block, p_max=b.p_max,
+                        weights=b.weights, dtype=np.dtype(b.dtype).name) for b in blocks]
         dH = torch.cat([p[0] for p in parts])
         dV0 = torch.cat([p[1] for p in parts])
         dA = torch.cat([p[2] for p in parts])

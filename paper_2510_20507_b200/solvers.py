@@ -374,6 +374,31 @@ class AmmmseEngine:
             raise NativeLibraryError(f"ammmse_generate_iid failed: {_native.error_string(rc)}")
         return H, V0, A
 
+    def generate_kronecker(self, B: int, K: int, N: int, M: int, d: int, *, seed0: int = 0,
+                           p_max: float = 10.0, weights: str = "ones", rho: float = 0.5,
+                           dtype="complex64", stream=None):
+        """On-device Kronecker-correlated batch (BASELINE configs[3]):
+        H_k = sqrt(beta_k) G_k R^{1/2} with G_k i.i.d. CN(0,1) from
+        ammmse_generate_iid, R_ij = rho^|i-j| (symmetric PSD root by eigh on the
+        host, inputs.kronecker_root), beta_k = 10^U[-2,0) from a second Philox
+        stream (seed tag 0xBE7A); V0 / weights as generate_iid.  The R^{1/2}
+        product is one batched library GEMM (input generation, not the solve)."""
+        torch = _torch()
+        from .inputs import kronecker_root
+
+        H, V0, A = self.generate_iid(B, K, N, M, d, seed0=seed0, p_max=p_max, weights=weights,
+                                     dtype=dtype, stream=stream)
+        _, _, U = self.generate_iid(B, K, 1, 1, 1, seed0=(int(seed0) ^ 0xBE7A) << 20, p_max=1.0,
+                                    weights="uniform", dtype=dtype, stream=stream)
+        beta = torch.pow(10.0, 2.0 * (U - 1.5))  # U in [0.5, 1.5) -> beta in [0.01, 1)
+        root = torch.from_numpy(kronecker_root(M, rho)).to(device=self.device, dtype=H.dtype)
+        cs = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(
+            torch.cuda.current_stream(self.device))
+        with cs:
+            H = torch.matmul(H.reshape(B * K * N, M), root).reshape(B, K, N, M)
+            H *= torch.sqrt(beta).to(H.real.dtype)[:, :, None, None]
+        return H.contiguous(), V0, A
+
     _RESULT_FIELDS = ("final_precoders", "wsr_bits", "iterations", "converged",
                       "stationarity_residual", "switch_iteration", "status")
 

@@ -68,3 +68,32 @@ def test_solver_parity_on_device_generated_inputs(cuda):
     assert np.array_equal(g.iterations, r["iterations"])
     assert np.array_equal(g.status, r["status"])
     np.testing.assert_allclose(g.wsr_bits, r["wsr_bits"], rtol=1e-9)
+
+
+def test_kronecker_generation(cuda):
+    """H_k = sqrt(beta_k) G_k R^{1/2}: undoing R^{1/2} leaves white rows whose
+    power is beta_k, log-uniform over [0.01, 1); deterministic in the seed."""
+    import torch
+
+    from paper_2510_20507_b200.inputs import kronecker_root
+
+    B, K, N, M = 512, 3, 2, 16
+    eng = AmmmseEngine(cuda)
+    H, V0, A = eng.generate_kronecker(B, K, N, M, 2, seed0=5, p_max=10.0, dtype="complex128")
+    torch.cuda.synchronize()
+    H = H.cpu().numpy()
+    np.testing.assert_array_equal(A.cpu().numpy(), 1.0)
+    # undo the correlation: G = H R^{-1/2} / sqrt(beta) must be white with equal row power
+    root = kronecker_root(M)
+    G = H @ np.linalg.inv(root)
+    p = np.mean(np.abs(G) ** 2, axis=(2, 3))  # (B, K) = beta_k
+    assert (p > 0.004).all() and (p < 1.6).all()
+    lb = np.log10(p).ravel()
+    # per-(b, k) power estimated from N M = 32 samples: allow the chi-square spread
+    assert -2.7 < lb.min() and lb.max() < 0.35 and abs(lb.mean() + 1.0) < 0.1
+    Gn = G / np.sqrt(p)[:, :, None, None]
+    C = np.einsum("bkni,bknj->ij", Gn, Gn.conj()) / (B * K * N)
+    np.testing.assert_allclose(C, np.eye(M), atol=0.08)
+    # deterministic
+    H2 = eng.generate_kronecker(B, K, N, M, 2, seed0=5, p_max=10.0, dtype="complex128")[0]
+    np.testing.assert_array_equal(H, H2.cpu().numpy())
