@@ -263,6 +263,12 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   }
   const void* func = plan.cluster ? (plan.tc ? plan.e->cluster_solve_tc : plan.e->cluster_solve)
                                   : plan.e->solve;
+  {  // shape-specialised single-CTA kernel (AMMMSE_NO_SPEC=1 disables it, for A/B)
+    const char* ns = getenv("AMMMSE_NO_SPEC");
+    if (!plan.cluster && plan.e->solve_spec && dims->M == plan.e->spec_M &&
+        dims->K == plan.e->spec_K && plan.threads == ammmse::kMaxThreads && !(ns && ns[0] == '1'))
+      func = plan.e->solve_spec;
+  }
   if (!func) {
     snprintf(g_err, sizeof g_err, "no kernel instantiation for this plan");
     return AMMMSE_ERR_UNSUPPORTED;

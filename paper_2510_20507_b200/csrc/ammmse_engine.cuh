@@ -1248,15 +1248,19 @@ struct Engine {
   }
 };
 
-template <typename R, int NN, int DD>
+// MC, KC != 0: shape-specialised instantiation (M = MC, K = KC, 256 threads),
+// so tile plans, split factors, loop trip counts and index arithmetic fold to
+// constants (the planner selects it when the dims match, entries.h).
+template <typename R, int NN, int DD, int MC = 0, int KC = 0>
 __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1) ammmse_solve_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
+  if constexpr (MC > 0) __builtin_assume(blockDim.x == kMaxThreads);
   Engine<R, NN, DD> e;
-  e.bind(smem, a.M, a.K);
+  const int M = MC > 0 ? MC : a.M, K = KC > 0 ? KC : a.K, KN = K * NN, KD = K * DD;
+  e.bind(smem, M, K);
   const int tid = threadIdx.x;
-  const int M = a.M, K = a.K, KN = K * NN, KD = K * DD;
   const int ldh = e.L.ldh, ldv = e.L.ldv, ldg = e.L.ldg;
   PhaseClock pc;
   pc.init(a.prof);

@@ -11,6 +11,8 @@ struct KernelEntry {
   const void* cluster_solve;                   // ammmse_cluster_kernel<R, N, d> (1 cluster / realization)
   size_t (*cluster_smem_bytes)(int M, int K, int C, int hres, int vglob, int sb, int tc);  // CLayout::bytes
   const void* cluster_solve_tc;                // ammmse_cluster_kernel<float, N, d, true> (nullptr for fp64)
+  const void* solve_spec = nullptr;            // ammmse_solve_kernel<R, N, d, spec_M, spec_K> (256 threads)
+  int spec_M = 0, spec_K = 0;
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4

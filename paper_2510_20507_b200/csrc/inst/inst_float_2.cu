@@ -19,8 +19,10 @@ size_t smem_fn(int M, int K) {
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>,
      (const void*)ammmse_cluster_kernel<float, 2, 1>, cluster_smem_fn<1>, (const void*)ammmse_cluster_kernel<float, 2, 1, true>},
+    // d = 2 carries the M = 64, K = 16 specialisation (BASELINE medium / sweep M = 64)
     {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>,
-     (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>, (const void*)ammmse_cluster_kernel<float, 2, 2, true>},
+     (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>, (const void*)ammmse_cluster_kernel<float, 2, 2, true>,
+     (const void*)ammmse_solve_kernel<float, 2, 2, 64, 16>, 64, 16},
     {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>,
      (const void*)ammmse_cluster_kernel<float, 2, 3>, cluster_smem_fn<3>, (const void*)ammmse_cluster_kernel<float, 2, 3, true>},
     {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>,
