@@ -265,9 +265,15 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
                                   : plan.e->solve;
   {  // shape-specialised single-CTA kernel (AMMMSE_NO_SPEC=1 disables it, for A/B)
     const char* ns = getenv("AMMMSE_NO_SPEC");
-    if (!plan.cluster && plan.e->solve_spec && dims->M == plan.e->spec_M &&
-        dims->K == plan.e->spec_K && plan.threads == ammmse::kMaxThreads && !(ns && ns[0] == '1'))
+    const bool use_spec = !(ns && ns[0] == '1');
+    if (use_spec && !plan.cluster && plan.e->solve_spec && dims->M == plan.e->spec_M &&
+        dims->K == plan.e->spec_K && plan.threads == ammmse::kMaxThreads)
       func = plan.e->solve_spec;
+    if (use_spec && plan.cluster && !plan.tc && plan.threads == 256)
+      for (int i = 0; i < plan.e->n_cluster_specs; ++i) {
+        const ammmse::SpecEntry& sp = plan.e->cluster_specs[i];
+        if (sp.M == dims->M && sp.K == dims->K && sp.C == plan.cluster) func = sp.f;
+      }
   }
   if (!func) {
     snprintf(g_err, sizeof g_err, "no kernel instantiation for this plan");

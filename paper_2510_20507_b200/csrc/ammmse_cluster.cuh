@@ -405,18 +405,22 @@ struct CLayout {
 
 // TC = true: the tcgen05 GEMM variant (separate instantiation, so the FFMA
 // kernel carries none of its code, registers or local arrays).
-template <typename R, int NN, int DD, bool TC = false>
+// MC, KC, CC != 0: shape-specialised instantiation (M, K, cluster size and
+// the 256-thread block known at compile time; the planner selects it when the
+// dims and its plan match, entries.h).
+template <typename R, int NN, int DD, bool TC = false, int MC = 0, int KC = 0, int CC = 0>
 __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
+  if constexpr (MC > 0) __builtin_assume(blockDim.x == kClusterThreads<NN, DD>);
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
-  const int C = (int)cl.num_blocks();
+  const int C = CC > 0 ? CC : (int)cl.num_blocks();
   const int tid = threadIdx.x;
 
   CLayout<R, NN, DD> L;
-  L.init(a.M, a.K, C, a.hres, a.vold_glob, a.sb_bytes, a.tcm);
+  L.init(MC > 0 ? MC : a.M, KC > 0 ? KC : a.K, C, a.hres, a.vold_glob, a.sb_bytes, a.tcm);
   const bool hres = a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;

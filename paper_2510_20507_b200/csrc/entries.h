@@ -4,6 +4,11 @@
 
 namespace ammmse {
 
+struct SpecEntry {  // shape-specialised cluster kernel: ammmse_cluster_kernel<R, N, d, false, M, K, C>
+  const void* f;
+  int M, K, C;
+};
+
 struct KernelEntry {
   const void* solve;                           // ammmse_solve_kernel<R, N, d>   (1 CTA / realization)
   const void* bounds;                          // ammmse_bounds_kernel<R, N>
@@ -13,6 +18,8 @@ struct KernelEntry {
   const void* cluster_solve_tc;                // ammmse_cluster_kernel<float, N, d, true> (nullptr for fp64)
   const void* solve_spec = nullptr;            // ammmse_solve_kernel<R, N, d, spec_M, spec_K> (256 threads)
   int spec_M = 0, spec_K = 0;
+  const SpecEntry* cluster_specs = nullptr;    // FFMA cluster kernels for fixed (M, K, C)
+  int n_cluster_specs = 0;
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4
