@@ -266,13 +266,16 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   {  // shape-specialised single-CTA kernel (AMMMSE_NO_SPEC=1 disables it, for A/B)
     const char* ns = getenv("AMMMSE_NO_SPEC");
     const bool use_spec = !(ns && ns[0] == '1');
-    if (use_spec && !plan.cluster && plan.e->solve_spec && dims->M == plan.e->spec_M &&
-        dims->K == plan.e->spec_K && plan.threads == ammmse::kMaxThreads)
-      func = plan.e->solve_spec;
-    if (use_spec && plan.cluster && !plan.tc && plan.threads == 256)
+    if (use_spec && !plan.cluster)
+      for (int i = 0; i < plan.e->n_solve_specs; ++i) {
+        const ammmse::SpecEntry& sp = plan.e->solve_specs[i];
+        if (sp.M == dims->M && sp.K == dims->K && sp.T == plan.threads) func = sp.f;
+      }
+    if (use_spec && plan.cluster && !plan.tc)
       for (int i = 0; i < plan.e->n_cluster_specs; ++i) {
         const ammmse::SpecEntry& sp = plan.e->cluster_specs[i];
-        if (sp.M == dims->M && sp.K == dims->K && sp.C == plan.cluster) func = sp.f;
+        if (sp.M == dims->M && sp.K == dims->K && sp.C == plan.cluster && sp.T == plan.threads)
+          func = sp.f;
       }
   }
   if (!func) {

@@ -1248,15 +1248,15 @@ struct Engine {
   }
 };
 
-// MC, KC != 0: shape-specialised instantiation (M = MC, K = KC, 256 threads),
+// MC, KC != 0: shape-specialised instantiation (M = MC, K = KC, NT threads),
 // so tile plans, split factors, loop trip counts and index arithmetic fold to
 // constants (the planner selects it when the dims match, entries.h).
-template <typename R, int NN, int DD, int MC = 0, int KC = 0>
+template <typename R, int NN, int DD, int MC = 0, int KC = 0, int NT = kMaxThreads>
 __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1) ammmse_solve_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
-  if constexpr (MC > 0) __builtin_assume(blockDim.x == kMaxThreads);
+  if constexpr (MC > 0) __builtin_assume(blockDim.x == NT);
   Engine<R, NN, DD> e;
   const int M = MC > 0 ? MC : a.M, K = KC > 0 ? KC : a.K, KN = K * NN, KD = K * DD;
   e.bind(smem, M, K);

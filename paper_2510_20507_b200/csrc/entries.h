@@ -4,9 +4,9 @@
 
 namespace ammmse {
 
-struct SpecEntry {  // shape-specialised cluster kernel: ammmse_cluster_kernel<R, N, d, false, M, K, C>
+struct SpecEntry {  // shape-specialised kernel for fixed (M, K, cluster size C, block size T)
   const void* f;
-  int M, K, C;
+  int M, K, C, T;
 };
 
 struct KernelEntry {
@@ -16,9 +16,9 @@ struct KernelEntry {
   const void* cluster_solve;                   // ammmse_cluster_kernel<R, N, d> (1 cluster / realization)
   size_t (*cluster_smem_bytes)(int M, int K, int C, int hres, int vglob, int sb, int tc);  // CLayout::bytes
   const void* cluster_solve_tc;                // ammmse_cluster_kernel<float, N, d, true> (nullptr for fp64)
-  const void* solve_spec = nullptr;            // ammmse_solve_kernel<R, N, d, spec_M, spec_K> (256 threads)
-  int spec_M = 0, spec_K = 0;
-  const SpecEntry* cluster_specs = nullptr;    // FFMA cluster kernels for fixed (M, K, C)
+  const SpecEntry* solve_specs = nullptr;      // ammmse_solve_kernel<R, N, d, M, K, T> (C = 0)
+  int n_solve_specs = 0;
+  const SpecEntry* cluster_specs = nullptr;    // FFMA cluster kernels for fixed (M, K, C), T = 256
   int n_cluster_specs = 0;
 };
 

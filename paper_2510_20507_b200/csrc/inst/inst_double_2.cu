@@ -16,11 +16,15 @@ size_t smem_fn(int M, int K) {
   L.init(M, K);
   return L.bytes;
 }
+// single-CTA engine: BASELINE small case (M=16, K=4, complex128, 64 threads)
+const SpecEntry kSolveSpecs22[1] = {
+    {(const void*)ammmse_solve_kernel<double, 2, 2, 16, 4, 64>, 16, 4, 0, 64},
+};
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<double, 2, 1>, (const void*)ammmse_bounds_kernel<double, 2>, smem_fn<1>,
      (const void*)ammmse_cluster_kernel<double, 2, 1>, cluster_smem_fn<1>, nullptr},
     {(const void*)ammmse_solve_kernel<double, 2, 2>, (const void*)ammmse_bounds_kernel<double, 2>, smem_fn<2>,
-     (const void*)ammmse_cluster_kernel<double, 2, 2>, cluster_smem_fn<2>, nullptr},
+     (const void*)ammmse_cluster_kernel<double, 2, 2>, cluster_smem_fn<2>, nullptr, kSolveSpecs22, 1},
     {(const void*)ammmse_solve_kernel<double, 2, 3>, (const void*)ammmse_bounds_kernel<double, 2>, smem_fn<3>,
      (const void*)ammmse_cluster_kernel<double, 2, 3>, cluster_smem_fn<3>, nullptr},
     {(const void*)ammmse_solve_kernel<double, 2, 4>, (const void*)ammmse_bounds_kernel<double, 2>, smem_fn<4>,

@@ -19,9 +19,14 @@ size_t smem_fn(int M, int K) {
 // BASELINE shapes on the cluster engine: massive / sweep M=256 (C=4), sweep M=128 (C=1),
 // sweep M=512 (C=16)
 const SpecEntry kClusterSpecs22[3] = {
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 256, 64, 4>, 256, 64, 4},
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 128, 32, 1>, 128, 32, 1},
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 512, 128, 16>, 512, 128, 16},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 256, 64, 4>, 256, 64, 4, 256},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 128, 32, 1>, 128, 32, 1, 256},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 512, 128, 16>, 512, 128, 16, 256},
+};
+// single-CTA engine: medium / sweep M=64 (256 threads), sweep M=32 (128 threads)
+const SpecEntry kSolveSpecs22[2] = {
+    {(const void*)ammmse_solve_kernel<float, 2, 2, 64, 16, 256>, 64, 16, 0, 256},
+    {(const void*)ammmse_solve_kernel<float, 2, 2, 32, 8, 128>, 32, 8, 0, 128},
 };
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<float, 2, 1>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<1>,
@@ -29,7 +34,7 @@ const KernelEntry kEntries[4] = {
     // d = 2 carries the M = 64, K = 16 specialisation (BASELINE medium / sweep M = 64)
     {(const void*)ammmse_solve_kernel<float, 2, 2>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<2>,
      (const void*)ammmse_cluster_kernel<float, 2, 2>, cluster_smem_fn<2>, (const void*)ammmse_cluster_kernel<float, 2, 2, true>,
-     (const void*)ammmse_solve_kernel<float, 2, 2, 64, 16>, 64, 16, kClusterSpecs22, 3},
+     kSolveSpecs22, 2, kClusterSpecs22, 3},
     {(const void*)ammmse_solve_kernel<float, 2, 3>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<3>,
      (const void*)ammmse_cluster_kernel<float, 2, 3>, cluster_smem_fn<3>, (const void*)ammmse_cluster_kernel<float, 2, 3, true>},
     {(const void*)ammmse_solve_kernel<float, 2, 4>, (const void*)ammmse_bounds_kernel<float, 2>, smem_fn<4>,
