@@ -324,11 +324,14 @@ def main():
                           "stationarity_residual", "switch_iteration", "status")}
         dbufs = [torch.empty_like(x, device=dev) for x in (hH, hs2, hP, hA, hV0)]
 
+        # slices of at least 2048 realizations (a tiny batch is one launch)
+        e2e_chunks = max(1, min(args.e2e_chunks, B // 2048))
+
         def e2e_step():
             # public API, host buffers: H2D of slice i+1 and D2H of slice i-1
             # overlap the solve of slice i (AmmmseEngine.solve_host)
             r = eng.solve_host((hH, hs2, hP, hA, hV0), hout, dbufs, res, stream=stream,
-                               chunks=args.e2e_chunks, **kw)
+                               chunks=e2e_chunks, **kw)
             if world > 1:
                 local_res = torch.stack([r.wsr_bits, r.iterations.to(torch.float64)], dim=1)
                 dist.all_gather_into_tensor(gather_buf.view(world * B, 2), local_res)

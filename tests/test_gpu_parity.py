@@ -261,3 +261,24 @@ def test_pipelined_host_solve_matches_device_solve(cuda, chunks):
     torch.cuda.synchronize()
     for f in AmmmseEngine._RESULT_FIELDS:
         np.testing.assert_array_equal(hout[f].numpy(), getattr(ref, f), err_msg=f)
+
+
+@pytest.mark.parametrize("shape", [(64, 2, 16, 2, 0), (32, 2, 8, 2, 0), (256, 2, 64, 2, 1)])
+def test_specialised_kernels_match_generic(cuda, shape, monkeypatch):
+    """The shape-specialised instantiations (entries.h) against the generic
+    kernels on the same inputs (AMMMSE_NO_SPEC=1): same iterations / status,
+    WSR and precoders to fp32 rounding."""
+    M, N, K, d, cl = shape
+    b = build_batch(M, N, K, d, 12 if cl else 24, p_max=100.0, weights="uniform",
+                    dtype=np.complex64)
+    opts = SolverOptions(algorithm="ammmse", gamma=0.002, omega=0.8, eps2=1e-5, max_iters=80)
+    run = lambda: run_ammmse_batch(b.channels, b.noise_power, b.p_max, b.weights, b.init_precoders,
+                                   opts)
+    monkeypatch.setenv("AMMMSE_NO_SPEC", "1")
+    gen = run()
+    monkeypatch.setenv("AMMMSE_NO_SPEC", "0")
+    spec = run()
+    assert np.array_equal(gen.status, spec.status)
+    assert np.array_equal(gen.iterations, spec.iterations)
+    np.testing.assert_allclose(spec.wsr_bits, gen.wsr_bits, rtol=1e-5)
+    np.testing.assert_allclose(spec.final_precoders, gen.final_precoders, rtol=0, atol=1e-4)
