@@ -1251,8 +1251,10 @@ struct Engine {
 // MC, KC != 0: shape-specialised instantiation (M = MC, K = KC, NT threads),
 // so tile plans, split factors, loop trip counts and index arithmetic fold to
 // constants (the planner selects it when the dims match, entries.h).
-template <typename R, int NN, int DD, int MC = 0, int KC = 0, int NT = kMaxThreads>
-__global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? AMMMSE_MINB : 1) ammmse_solve_kernel(EngineArgs a) {
+// MB: resident CTAs per SM the register budget is sized for (N d <= 4).
+template <typename R, int NN, int DD, int MC = 0, int KC = 0, int NT = kMaxThreads,
+          int MB = AMMMSE_MINB>
+__global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? MB : 1) ammmse_solve_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
   __shared__ unsigned long long s_r;
