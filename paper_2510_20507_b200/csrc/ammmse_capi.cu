@@ -274,7 +274,9 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     if (use_spec && plan.cluster && !plan.tc)
       for (int i = 0; i < plan.e->n_cluster_specs; ++i) {
         const ammmse::SpecEntry& sp = plan.e->cluster_specs[i];
-        if (sp.M == dims->M && sp.K == dims->K && sp.C == plan.cluster && sp.T == plan.threads)
+        const bool place_ok = sp.sb == 0 || (!plan.hres && plan.vglob && plan.sb == sp.sb);
+        if (sp.M == dims->M && sp.K == dims->K && sp.C == plan.cluster && sp.T == plan.threads &&
+            place_ok)
           func = sp.f;
       }
   }

@@ -408,7 +408,10 @@ struct CLayout {
 // MC, KC, CC != 0: shape-specialised instantiation (M, K, cluster size and
 // the 256-thread block known at compile time; the planner selects it when the
 // dims and its plan match, entries.h).
-template <typename R, int NN, int DD, bool TC = false, int MC = 0, int KC = 0, int CC = 0>
+// SBC != 0 (specialisations only): the plan's placement is fixed too (H streamed,
+// V_old in the global slot, SBC-byte staging buffers).
+template <typename R, int NN, int DD, bool TC = false, int MC = 0, int KC = 0, int CC = 0,
+          int SBC = 0>
 __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_kernel(EngineArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Ctl ctl;
@@ -420,8 +423,9 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   const int tid = threadIdx.x;
 
   CLayout<R, NN, DD> L;
-  L.init(MC > 0 ? MC : a.M, KC > 0 ? KC : a.K, C, a.hres, a.vold_glob, a.sb_bytes, a.tcm);
-  const bool hres = a.hres != 0;
+  L.init(MC > 0 ? MC : a.M, KC > 0 ? KC : a.K, C, SBC > 0 ? 0 : a.hres, SBC > 0 ? 1 : a.vold_glob,
+         SBC > 0 ? SBC : a.sb_bytes, a.tcm);
+  const bool hres = SBC > 0 ? false : a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
   const int k0 = crank * KL;       // first own user

@@ -7,6 +7,7 @@ namespace ammmse {
 struct SpecEntry {  // shape-specialised kernel for fixed (M, K, cluster size C, block size T)
   const void* f;
   int M, K, C, T;
+  int sb = 0;  // cluster: > 0 = compiled for the streamed-H / global-V_old plan with sb-byte stages
 };
 
 struct KernelEntry {

@@ -18,10 +18,11 @@ size_t smem_fn(int M, int K) {
 }
 // BASELINE shapes on the cluster engine: massive / sweep M=256 (C=4), sweep M=128 (C=1),
 // sweep M=512 (C=16)
+// (placement fixed to the planner's choice for these shapes: H streamed, V_old in L2)
 const SpecEntry kClusterSpecs22[3] = {
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 256, 64, 4>, 256, 64, 4, 256},
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 128, 32, 1>, 128, 32, 1, 256},
-    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 512, 128, 16>, 512, 128, 16, 256},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 256, 64, 4, 20480>, 256, 64, 4, 256, 20480},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 128, 32, 1, 20480>, 128, 32, 1, 256, 20480},
+    {(const void*)ammmse_cluster_kernel<float, 2, 2, false, 512, 128, 16, 12288>, 512, 128, 16, 256, 12288},
 };
 // single-CTA engine: medium / sweep M=64 (256 threads; registers sized for 2 CTAs/SM,
 // 128 regs without spills, measured +2 % over 3 CTAs/SM at 80 regs), sweep M=32

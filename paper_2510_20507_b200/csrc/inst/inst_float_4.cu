@@ -18,7 +18,7 @@ size_t smem_fn(int M, int K) {
 }
 // BASELINE large case on the cluster engine: M=128, K=32, N=d=4 (C=4)
 const SpecEntry kClusterSpecs44[1] = {
-    {(const void*)ammmse_cluster_kernel<float, 4, 4, false, 128, 32, 4>, 128, 32, 4, 256},
+    {(const void*)ammmse_cluster_kernel<float, 4, 4, false, 128, 32, 4, 20480>, 128, 32, 4, 256, 20480},
 };
 const KernelEntry kEntries[4] = {
     {(const void*)ammmse_solve_kernel<float, 4, 1>, (const void*)ammmse_bounds_kernel<float, 4>, smem_fn<1>,
