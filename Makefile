@@ -1,7 +1,9 @@
 # Builds the in-tree engine library paper_2510_20507_b200/libammmse.so for sm_100a.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
+# PHASES=1: diagnostic build with the per-phase clock64 timers (ammmse_phase_profile)
+PHASES ?= 0
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v -DAMMMSE_PHASES=$(PHASES)
 SRC_DIR := paper_2510_20507_b200/csrc
 OBJ_DIR := build/obj
 SRCS := $(SRC_DIR)/ammmse_capi.cu $(SRC_DIR)/ammmse_gen.cu $(wildcard $(SRC_DIR)/inst/*.cu)

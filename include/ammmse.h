@@ -181,14 +181,16 @@ int ammmse_generate_iid(const AmmmseDims* dims, unsigned long long seed0, double
                         int uniform_weights, void* channels, void* init_precoders,
                         double* weights, void* stream);
 
-/* Diagnostics (no reference counterpart).  When the environment variable
-   AMMMSE_PROFILE_PHASES=1 is set, ammmse_solve synchronises its stream and
-   records per-phase shares of the solve kernel's CTA-cycles (thread 0 clock64
-   deltas).  Copies up to n shares of the last profiled solve into `shares`
-   and returns the number of phases (0 if none); *bcgd_first / *bcgd_count
-   name the phases of the BCGD precoder step (GEMM-A + step + projection,
-   GEMM-B). */
-int ammmse_last_phase_profile(double* shares, int n, int* bcgd_first, int* bcgd_count);
+/* Diagnostics (no reference counterpart).  In a library built with
+   AMMMSE_PHASES=1 (`make PHASES=1`), ammmse_solve run with the environment
+   variable AMMMSE_PROFILE_PHASES=1 accumulates per-phase thread-0 clock64
+   totals of the solve kernel into the call's workspace.  This copies them
+   back (synchronising `stream`), writes up to n shares into `shares` and
+   returns the number of phases (0 in production builds or when nothing was
+   recorded); *bcgd_first / *bcgd_count name the phases of the BCGD precoder
+   step (GEMM-A + step + projection, GEMM-B).  No library-global state. */
+int ammmse_phase_profile(const void* workspace, double* shares, int n, int* bcgd_first,
+                         int* bcgd_count, void* stream);
 
 #ifdef __cplusplus
 }

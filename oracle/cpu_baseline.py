@@ -12,6 +12,7 @@ imported (SURVEY.md §8(d) CPU path timing).
 
 from __future__ import annotations
 
+import math
 import multiprocessing as mp
 import os
 import time
@@ -28,7 +29,22 @@ def _solve_task(task):
     H, s2, alpha, p_max, V0, opts = task
     o = orc.solve(np.asarray(H, dtype=np.complex128), s2, alpha, p_max,
                   np.asarray(V0, dtype=np.complex128), **opts)
-    return o["wsr_bits"], o["iterations"], o["status"]
+    return (o["wsr_bits"], o["iterations"], o["status"], o["switch_iteration"],
+            marginal(o["trace"][:, 8], opts.get("eps1", 0.1), opts.get("eps2", 1e-3)))
+
+
+MARGIN = 1e-2  # |rel - eps| <= 1e-2 eps is a marginal stop / switch decision
+
+
+def marginal(rel, eps1, eps2) -> bool:
+    """True if any rel_change of the trace lies within ±1 % of eps1 or eps2,
+    i.e. the iteration / switch count is not a robust comparison point."""
+    import numpy as np
+
+    rel = np.asarray(rel, dtype=np.float64)
+    rel = rel[np.isfinite(rel)]
+    near = lambda eps: math.isfinite(eps) and bool(np.any(np.abs(rel - eps) <= MARGIN * eps))
+    return near(eps1) or near(eps2)
 
 
 def _warm(_):

@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "ammmse_solve",
     "ammmse_bounds",
     "ammmse_error_string",
-    "ammmse_last_phase_profile",
+    "ammmse_phase_profile",
     "ammmse_generate_iid",
 )
 
@@ -92,10 +92,10 @@ def lib() -> ctypes.CDLL:
         h.ammmse_generate_iid.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.c_ulonglong,
                                           ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
-        h.ammmse_last_phase_profile.restype = ctypes.c_int
-        h.ammmse_last_phase_profile.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
-                                                ctypes.POINTER(ctypes.c_int),
-                                                ctypes.POINTER(ctypes.c_int)]
+        h.ammmse_phase_profile.restype = ctypes.c_int
+        h.ammmse_phase_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int), ctypes.c_void_p]
         h.ammmse_abi_version.restype = ctypes.c_int
         h.ammmse_abi_version.argtypes = []
         h.ammmse_check_dims.restype = ctypes.c_int

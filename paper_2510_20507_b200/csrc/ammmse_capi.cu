@@ -18,10 +18,12 @@
 
 namespace {
 
-thread_local char g_err[256];
-// last AMMMSE_PROFILE_PHASES solve (diagnostics)
-static double g_phase_share[16];
-static int g_phase_n = 0;
+thread_local char g_err[256];  // per-thread text of the last error (ammmse_error_string)
+
+// workspace layout: [0, 8) persistent-kernel work counter, [64, 192) phase
+// counters (diagnostic builds), scratch from byte 256
+constexpr size_t kPhaseOff = 64;
+constexpr int kPhaseN = 10;
 
 const ammmse::KernelEntry* lookup(const AmmmseDims* d) {
   if (d->N < 1 || d->N > 4 || d->d < 1 || d->d > 4) return nullptr;
@@ -320,6 +322,9 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
       return AMMMSE_ERR_UNSUPPORTED;
     }
     long long nc = nclusters < dims->batch ? nclusters : dims->batch;
+    // per-CTA global scratch slots (V_old, tensor-core H planes) are sized for
+    // at most one CTA per SM (scratch_bytes): never launch more
+    if ((plan.vglob || plan.tc) && nc * plan.cluster > sms) nc = sms / plan.cluster;
     grid = nc * plan.cluster;
     cfg.gridDim = dim3((unsigned)grid);
   } else {
@@ -380,14 +385,15 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     a.hplanes = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(workspace) + 256 + off);
   }
   a.counter = reinterpret_cast<unsigned long long*>(workspace);
-  // debug: per-phase clock totals (AMMMSE_PROFILE_PHASES=1), printed to stderr
-  static unsigned long long* prof_buf = nullptr;
-  const char* pe = getenv("AMMMSE_PROFILE_PHASES");
-  const bool profile = pe && pe[0] == '1';
-  if (profile) {
-    if (!prof_buf) cudaMalloc(&prof_buf, 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(prof_buf, 0, 16 * sizeof(unsigned long long), s);
-    a.prof = prof_buf;
+  // diagnostic builds (AMMMSE_PHASES=1) with AMMMSE_PROFILE_PHASES=1: per-phase
+  // thread-0 clock64 totals into the caller's workspace (ammmse_phase_profile)
+  if (AMMMSE_PHASES) {
+    const char* pe = getenv("AMMMSE_PROFILE_PHASES");
+    if (pe && pe[0] == '1') {
+      a.prof = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(workspace) + kPhaseOff);
+      ce = cudaMemsetAsync(a.prof, 0, kPhaseN * sizeof(unsigned long long), s);
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync(phases)");
+    }
   }
   void* args[] = {&a};
   if (plan.cluster)
@@ -395,28 +401,26 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   else
     ce = cudaLaunchKernel(func, dim3((unsigned)grid), dim3(threads), args, smem, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "kernel launch (solve)");
-  if (profile) {
-    unsigned long long h[16];
-    cudaMemcpyAsync(h, prof_buf, sizeof h, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    double tot = 0;
-    for (int i = 0; i < 10; ++i) tot += (double)h[i];
-    for (int i = 0; i < 10; ++i) g_phase_share[i] = tot > 0 ? (double)h[i] / tot : 0.0;
-    g_phase_n = 10;  // both engines: p2 = GEMM-A + step + projection, p3 = GEMM-B (+ Grams)
-    fprintf(stderr, "[ammmse phases] engine=%s C=%d hres=%d:", plan.cluster ? "cluster" : "single",
-            plan.cluster, plan.hres);
-    for (int i = 0; i < 10; ++i) fprintf(stderr, " p%d=%.1f%%", i, tot > 0 ? 100.0 * h[i] / tot : 0.0);
-    fprintf(stderr, " (total %.3g CTA-cycles)\n", tot);
-  }
   return AMMMSE_OK;
 }
 
-int ammmse_last_phase_profile(double* shares, int n, int* bcgd_first, int* bcgd_count) {
+int ammmse_phase_profile(const void* workspace, double* shares, int n, int* bcgd_first,
+                         int* bcgd_count, void* stream) {
   if (bcgd_first) *bcgd_first = 2;
   if (bcgd_count) *bcgd_count = 2;
+  if (!AMMMSE_PHASES) return 0;
+  if (!workspace) return AMMMSE_ERR_INVALID;
+  unsigned long long h[kPhaseN];
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t ce = cudaMemcpyAsync(h, reinterpret_cast<const unsigned char*>(workspace) + kPhaseOff,
+                                   sizeof h, cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "phase counters");
+  double tot = 0;
+  for (int i = 0; i < kPhaseN; ++i) tot += (double)h[i];
   if (shares)
-    for (int i = 0; i < n && i < g_phase_n; ++i) shares[i] = g_phase_share[i];
-  return g_phase_n;
+    for (int i = 0; i < n && i < kPhaseN; ++i) shares[i] = tot > 0 ? (double)h[i] / tot : 0.0;
+  return tot > 0 ? kPhaseN : 0;
 }
 
 int ammmse_bounds(const AmmmseDims* dims, const void* channels, const double* weights,

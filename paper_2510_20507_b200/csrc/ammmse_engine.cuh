@@ -140,8 +140,13 @@ struct Layout {
 };
 
 // Debug phase timers: thread 0 of every CTA accumulates clock64() deltas per
-// phase and adds them to EngineArgs::prof at exit (AMMMSE_PROFILE_PHASES=1).
+// phase and adds them to EngineArgs::prof at exit (built with AMMMSE_PHASES=1 and run
+// with AMMMSE_PROFILE_PHASES=1; the counters live in the caller's workspace).
 constexpr int kProfPhases = 10;
+#ifndef AMMMSE_PHASES
+#define AMMMSE_PHASES 0  // compile-time switch: production kernels carry no timers
+#endif
+#if AMMMSE_PHASES
 struct PhaseClock {
   unsigned long long* out;
   long long last;
@@ -165,6 +170,13 @@ struct PhaseClock {
       for (int i = 0; i < kProfPhases; ++i) atomicAdd(out + i, (unsigned long long)acc[i]);
   }
 };
+#else
+struct PhaseClock {
+  __device__ __forceinline__ void init(unsigned long long*) {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush() {}
+};
+#endif
 
 // Control block of the running realization (static shared memory).
 struct Ctl {

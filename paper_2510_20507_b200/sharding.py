@@ -51,6 +51,8 @@ def gather_scalars(local: np.ndarray, total: int, group=None, device=None) -> np
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if device is None and dist.get_backend(group) == "nccl":  # NCCL gathers device tensors
+        device = torch.device("cuda", torch.cuda.current_device())
     per = -(-total // world)
     F = local.shape[1]
     buf = torch.zeros((per, F), dtype=torch.float64, device=device)

@@ -241,8 +241,11 @@ class AmmmseEngine:
         if not torch.cuda.is_available():
             raise NativeLibraryError("the A-MMMSE engine needs a CUDA device (no CPU fallback)")
         self.lib = _native.lib()
-        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        self._ws = None
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dev.type != "cuda":
+            raise ConfigError(f"the engine runs on a CUDA device, got {dev}")
+        self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+        self._ws = {}
 
     def dims(self, channels, init_precoders) -> _native.AmmmseDims:
         torch = _torch()
@@ -268,11 +271,47 @@ class AmmmseEngine:
             raise ConfigError(f"shape (M={dims.M}, N={dims.N}, K={dims.K}, d={dims.d}) not supported "
                               f"by the engine: {_native.error_string(rc)}")
 
-    def _workspace(self, nbytes: int):
+    def _workspace(self, nbytes: int, stream=None):
+        """Engine-owned workspace, one per stream (it holds the persistent
+        kernel's work counter, so two solves in flight on different streams
+        must not share it).  Growing it first waits for the stream's pending
+        work on the old buffer."""
         torch = _torch()
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-        return self._ws
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        if not isinstance(self._ws, dict):
+            self._ws = {}
+        key = int(stream.cuda_stream)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            if ws is not None:
+                stream.synchronize()
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
+
+    def _check_out(self, out, init_precoders, B: int, max_iters: int) -> None:
+        """A caller-supplied result must match this call (the kernel writes B
+        entries of every field and (B, max_iters, 9) trace rows)."""
+        torch = _torch()
+        want = {"final_precoders": (tuple(init_precoders.shape), init_precoders.dtype),
+                "wsr_bits": ((B,), torch.float64), "iterations": ((B,), torch.int32),
+                "converged": ((B,), torch.uint8), "stationarity_residual": ((B,), torch.float64),
+                "switch_iteration": ((B,), torch.int32), "status": ((B,), torch.int32),
+                "gamma_used": ((B,), torch.float64)}
+        for f, (shape, dt) in want.items():
+            t = getattr(out, f)
+            if t is None:
+                continue
+            if (tuple(t.shape) != shape or t.dtype != dt or t.device != self.device
+                    or not t.is_contiguous()):
+                raise ConfigError(f"out.{f} must be a contiguous {dt} tensor of shape {shape} on "
+                                  f"{self.device}")
+        if out.trace is not None:
+            shape = (B, max_iters, _native.TRACE_FIELDS)
+            if (tuple(out.trace.shape) != shape or out.trace.dtype != torch.float64
+                    or out.trace.device != self.device or not out.trace.is_contiguous()):
+                raise ConfigError(f"out.trace must be a contiguous float64 tensor of shape {shape}")
 
     def solve(self, channels, noise_power, p_max, weights, init_precoders, *, gamma, omega,
               eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
@@ -282,12 +321,20 @@ class AmmmseEngine:
         dims = self.dims(channels, init_precoders)
         self.check(dims)
         B = dims.batch
-        dev = channels.device
-        for name, t in (("noise_power", noise_power), ("p_max", p_max), ("weights", weights)):
-            if t.dtype != torch.float64 or t.device != dev or not t.is_contiguous():
-                raise ConfigError(f"{name} must be a contiguous float64 tensor on {dev}")
+        dev = self.device
+        K = dims.K
+        if channels.device != dev or init_precoders.device != dev:
+            raise ConfigError(f"channels / init_precoders must live on the engine's device {dev}")
+        for name, t, shape in (("noise_power", noise_power, (B,)), ("p_max", p_max, (B,)),
+                               ("weights", weights, (B, K))):
+            if (t.dtype != torch.float64 or t.device != dev or not t.is_contiguous()
+                    or tuple(t.shape) != shape):
+                raise ConfigError(f"{name} must be a contiguous float64 tensor of shape {shape} "
+                                  f"on {dev}")
         if not channels.is_contiguous() or not init_precoders.is_contiguous():
             raise ConfigError("channels / init_precoders must be contiguous")
+        if out is not None:
+            self._check_out(out, init_precoders, B, int(max_iters))
         if out is None:
             out = BatchResult(
                 final_precoders=torch.empty_like(init_precoders),
@@ -326,18 +373,22 @@ class AmmmseEngine:
             ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
             ptr(out.stationarity_residual), ptr(out.switch_iteration), ptr(out.status),
             ptr(out.gamma_used), ptr(out.trace))
-        ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
-        if ws_bytes == 0:
-            raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
-                              f"h_placement={h_placement}, tensor_cores={tensor_cores})")
-        if workspace is not None and workspace.numel() >= ws_bytes:
-            ws = workspace  # caller-owned (concurrent solves on several streams)
-        else:
-            ws = self._workspace(ws_bytes)
-        if stream is None:
-            stream = torch.cuda.current_stream(dev)
-        rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
-                                   ctypes_stream(stream))
+        with torch.cuda.device(dev):  # the C-ABI launches on the current device
+            ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
+            if ws_bytes == 0:
+                raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
+                                  f"h_placement={h_placement}, tensor_cores={tensor_cores})")
+            if workspace is not None:
+                # caller-owned (concurrent solves on several streams each own one)
+                if workspace.device != dev or workspace.numel() < ws_bytes:
+                    raise ConfigError(f"workspace must be a tensor of >= {ws_bytes} bytes on {dev}")
+                ws = workspace
+            else:
+                ws = self._workspace(ws_bytes, stream)
+            if stream is None:
+                stream = torch.cuda.current_stream(dev)
+            rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
+                                       ctypes_stream(stream))
         if rc != 0:
             if rc == _native.ERR_INVALID:
                 raise ConfigError(_native.error_string(rc))
@@ -367,9 +418,10 @@ class AmmmseEngine:
                                   _native.COMPLEX64 if ct == torch.complex64 else _native.COMPLEX128)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
-        rc = self.lib.ammmse_generate_iid(dims, int(seed0), float(p_max),
-                                          1 if weights == "uniform" else 0, H.data_ptr(),
-                                          V0.data_ptr(), A.data_ptr(), ctypes_stream(stream))
+        with torch.cuda.device(dev):
+            rc = self.lib.ammmse_generate_iid(dims, int(seed0), float(p_max),
+                                              1 if weights == "uniform" else 0, H.data_ptr(),
+                                              V0.data_ptr(), A.data_ptr(), ctypes_stream(stream))
         if rc != 0:
             raise NativeLibraryError(f"ammmse_generate_iid failed: {_native.error_string(rc)}")
         return H, V0, A
@@ -459,14 +511,27 @@ class AmmmseEngine:
         """Batched compute_bounds (ref objective.py:216-240): (B, 5) float64
         [kappa, l_v, gamma_safe, ek_floor, alpha_bar]."""
         torch = _torch()
+        if channels.dim() != 4 or channels.dtype not in (torch.complex64, torch.complex128):
+            raise ConfigError("channels must be a (B, K, N, M) complex64 / complex128 tensor")
         B, K, N, M = channels.shape
+        dev = self.device
+        for name, t, shape in (("weights", weights, (B, K)), ("p_max", p_max, (B,)),
+                               ("noise_power", noise_power, (B,))):
+            if (t.dtype != torch.float64 or t.device != dev or not t.is_contiguous()
+                    or tuple(t.shape) != shape):
+                raise ConfigError(f"{name} must be a contiguous float64 tensor of shape {shape} "
+                                  f"on {dev}")
+        if channels.device != dev or not channels.is_contiguous():
+            raise ConfigError(f"channels must be contiguous on {dev}")
         dt = _native.COMPLEX64 if channels.dtype == torch.complex64 else _native.COMPLEX128
         dims = _native.AmmmseDims(B, M, N, K, 1, dt)
-        out = torch.empty((B, _native.BOUND_FIELDS), dtype=torch.float64, device=channels.device)
+        out = torch.empty((B, _native.BOUND_FIELDS), dtype=torch.float64, device=dev)
         if stream is None:
-            stream = torch.cuda.current_stream(channels.device)
-        rc = self.lib.ammmse_bounds(dims, channels.data_ptr(), weights.data_ptr(), p_max.data_ptr(),
-                                    noise_power.data_ptr(), out.data_ptr(), ctypes_stream(stream))
+            stream = torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev):
+            rc = self.lib.ammmse_bounds(dims, channels.data_ptr(), weights.data_ptr(),
+                                        p_max.data_ptr(), noise_power.data_ptr(), out.data_ptr(),
+                                        ctypes_stream(stream))
         if rc != 0:
             raise NativeLibraryError(f"ammmse_bounds failed: {_native.error_string(rc)}")
         return out
@@ -483,9 +548,10 @@ def engine(device=None) -> AmmmseEngine:
     torch = _torch()
     if not torch.cuda.is_available():
         raise NativeLibraryError("the A-MMMSE engine needs a CUDA device (no CPU fallback)")
-    key = torch.cuda.current_device() if device is None else torch.device(device).index
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = torch.cuda.current_device() if dev.index is None else dev.index
     if key not in _ENGINES:
-        _ENGINES[key] = AmmmseEngine(device)
+        _ENGINES[key] = AmmmseEngine(torch.device("cuda", key))
     return _ENGINES[key]
 
 
