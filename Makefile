@@ -12,8 +12,12 @@ HDRS := include/ammmse.h $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/entries.h
 LIB := paper_2510_20507_b200/libammmse.so
 PROBE := paper_2510_20507_b200/libammmse_probe.so
 TCTEST := paper_2510_20507_b200/libammmse_tctest.so
+GEMMSTEP := paper_2510_20507_b200/libammmse_gemmstep.so
 
-all: $(LIB) $(PROBE) $(TCTEST)
+all: $(LIB) $(PROBE) $(TCTEST) $(GEMMSTEP)
+
+$(GEMMSTEP): $(SRC_DIR)/tools/gemm_step.cu $(SRC_DIR)/tc_stream.cuh $(SRC_DIR)/tc_umma.cuh
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -shared -o $@ $<
 
 $(TCTEST): $(SRC_DIR)/tools/tc_selftest.cu $(SRC_DIR)/tc_umma.cuh
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -shared -o $@ $<
@@ -28,7 +32,22 @@ $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
-clean:
-	rm -rf build $(LIB) $(PROBE) $(TCTEST)
+# diagnostic library with the per-phase clock64 timers (ammmse_phase_profile);
+# load it with AMMMSE_LIB=paper_2510_20507_b200/libammmse_phases.so
+PHASES_OBJ := build/obj_phases
+PHASES_LIB := paper_2510_20507_b200/libammmse_phases.so
+PHASES_OBJS := $(patsubst $(SRC_DIR)/%.cu,$(PHASES_OBJ)/%.o,$(SRCS))
 
-.PHONY: all clean
+$(PHASES_OBJ)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -DAMMMSE_PHASES=1 -c $< -o $@
+
+$(PHASES_LIB): $(PHASES_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(PHASES_OBJS)
+
+phases: $(PHASES_LIB)
+
+clean:
+	rm -rf build $(LIB) $(PROBE) $(TCTEST) $(GEMMSTEP) $(PHASES_LIB)
+
+.PHONY: all clean phases

@@ -456,6 +456,11 @@ def main():
             dist.destroy_process_group()
         return
 
+    from paper_2510_20507_b200 import _native
+
+    engine_plan = _native.plan_info(eng.dims(dH, dV0), _native.AmmmseOptions(
+        max_iters=int(w.max_iters), cluster_size=args.cluster_size, h_placement=args.h_placement,
+        tensor_cores=args.tensor_cores))
     # ---- roofline of the (only) kernel: FMA pipe, GEMM-step flops ----
     import ctypes
 
@@ -549,6 +554,7 @@ def main():
         "data": ("synthetic, generated on the device (Philox4x32-10 CN(0,1), ammmse_generate_iid)"
                  if args.device_inputs else "synthetic (seeded Philox inputs, SURVEY.md §8(d))"),
         "config": {"workload": label, "M": w.M, "K": w.K, "N": w.N, "d": w.d,
+                   "engine": engine_plan,
                    "realizations_per_gpu_step": B, "snr_blocks": len(blocks),
                    "max_iters": w.max_iters, "eps2": w.eps2, "gamma": [b.gamma for b in blocks],
                    "omega": w.omega,

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define AMMMSE_ABI_VERSION 1
+#define AMMMSE_ABI_VERSION 2
 
 /* element type of channels / precoders */
 enum {
@@ -133,6 +133,13 @@ typedef struct AmmmseResult {
   double* gamma_used;             /* (B,)  resolved step size                      */
   double* trace;                  /* (B, max_iters, AMMMSE_TRACE_FIELDS), rows past
                                      `iterations` are left untouched              */
+  /* Recorded block iterates (SolverOptions.record_iterates, solvers.py:106, :487-488):
+     per completed iteration t the (U, W, V_new) the reference appends as
+     BlockIterate, complex128 (interleaved doubles) whatever the input dtype.
+     Rows past `iterations` are left untouched.  All three NULL = not recorded. */
+  double* iter_receivers;         /* (B, max_iters, K, N, d) complex128           */
+  double* iter_weights;           /* (B, max_iters, K, d, d) complex128           */
+  double* iter_precoders;         /* (B, max_iters, K, M, d) complex128           */
 } AmmmseResult;
 
 /* BoundsReport (objective.py:40-66) per realization, (B, 5) row-major */
@@ -180,6 +187,12 @@ const char* ammmse_error_string(int code);
 int ammmse_generate_iid(const AmmmseDims* dims, unsigned long long seed0, double p_max,
                         int uniform_weights, void* channels, void* init_precoders,
                         double* weights, void* stream);
+
+/* Diagnostics: the engine configuration ammmse_solve would launch for these
+   dims / options.  info[8] = {cluster size (0 = single-CTA engine), H resident,
+   V_old in global scratch, staging bytes, tensor-core GEMMs, shared memory bytes
+   per CTA, threads per CTA, shape-specialised kernel}. */
+int ammmse_plan_info(const AmmmseDims* dims, const AmmmseOptions* options, int* info);
 
 /* Diagnostics (no reference counterpart).  In a library built with
    AMMMSE_PHASES=1 (`make PHASES=1`), ammmse_solve run with the environment

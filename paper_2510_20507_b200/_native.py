@@ -16,7 +16,7 @@ from .errors import NativeLibraryError
 
 LIB_PATH = pathlib.Path(__file__).resolve().with_name("libammmse.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 COMPLEX64 = 0
 COMPLEX128 = 1
 TRACE_FIELDS = 9
@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "ammmse_bounds",
     "ammmse_error_string",
     "ammmse_phase_profile",
+    "ammmse_plan_info",
     "ammmse_generate_iid",
 )
 
@@ -67,7 +68,8 @@ class AmmmseResult(ctypes.Structure):
                 ("iterations", ctypes.c_void_p), ("converged", ctypes.c_void_p),
                 ("stationarity_residual", ctypes.c_void_p), ("switch_iteration", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("gamma_used", ctypes.c_void_p),
-                ("trace", ctypes.c_void_p)]
+                ("trace", ctypes.c_void_p), ("iter_receivers", ctypes.c_void_p),
+                ("iter_weights", ctypes.c_void_p), ("iter_precoders", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()
@@ -92,6 +94,9 @@ def lib() -> ctypes.CDLL:
         h.ammmse_generate_iid.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.c_ulonglong,
                                           ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        h.ammmse_plan_info.restype = ctypes.c_int
+        h.ammmse_plan_info.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.POINTER(AmmmseOptions),
+                                       ctypes.POINTER(ctypes.c_int)]
         h.ammmse_phase_profile.restype = ctypes.c_int
         h.ammmse_phase_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                            ctypes.c_int, ctypes.POINTER(ctypes.c_int),
@@ -122,3 +127,16 @@ def lib() -> ctypes.CDLL:
 
 def error_string(code: int) -> str:
     return lib().ammmse_error_string(int(code)).decode(errors="replace")
+
+
+PLAN_FIELDS = ("cluster", "h_resident", "vold_global", "stage_bytes", "tensor_cores", "smem_bytes",
+               "threads", "specialised")
+
+
+def plan_info(dims: AmmmseDims, options: AmmmseOptions | None = None) -> dict:
+    """The engine configuration ammmse_solve would launch (ammmse_plan_info)."""
+    info = (ctypes.c_int * 8)()
+    rc = lib().ammmse_plan_info(dims, options or AmmmseOptions(), info)
+    if rc != 0:
+        raise NativeLibraryError(f"ammmse_plan_info: {error_string(rc)}")
+    return dict(zip(PLAN_FIELDS, list(info)))

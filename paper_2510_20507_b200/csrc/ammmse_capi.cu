@@ -172,6 +172,12 @@ size_t tc_planes_bytes(const AmmmseDims* d, const Plan& p, int sms) {
   return (size_t)((sms + p.cluster - 1) / p.cluster) * per + 256;
 }
 
+// row stride of the per-CTA V_old slot (CLayout::ldv: padded in tensor-core mode)
+size_t vold_ld(const AmmmseDims* d, const Plan& p) {
+  const size_t ncol = (size_t)(d->K / p.cluster) * d->d;
+  return p.tc ? ncol + 1 : ncol;
+}
+
 // bytes of per-CTA V_old scratch (cluster engine, vglob plans); one CTA per SM
 // is resident for those plans, so the slot count is bounded by the SM count
 size_t scratch_bytes(const AmmmseDims* d, const Plan& p) {
@@ -181,9 +187,8 @@ size_t scratch_bytes(const AmmmseDims* d, const Plan& p) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
     sms = 160;
   const size_t rsz = d->dtype == AMMMSE_COMPLEX64 ? 4 : 8;
-  const size_t ncol = (size_t)(d->K / p.cluster) * d->d;
-  size_t b = p.vglob ? (size_t)sms * 2 * (size_t)d->M * ncol * rsz : 0;
-  if (p.tc) b += tc_planes_bytes(d, p, sms);
+  size_t b = p.vglob ? (size_t)sms * 2 * (size_t)d->M * vold_ld(d, p) * rsz : 0;
+  if (p.tc) b = ((b + 255) & ~(size_t)255) + tc_planes_bytes(d, p, sms);
   return b;
 }
 
@@ -360,6 +365,14 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.status = res->status;
   a.gamma_used = res->gamma_used;
   a.trace = res->trace;
+  if ((res->iter_receivers != nullptr) != (res->iter_weights != nullptr) ||
+      (res->iter_receivers != nullptr) != (res->iter_precoders != nullptr)) {
+    snprintf(g_err, sizeof g_err, "iterate buffers must be all set or all NULL");
+    return AMMMSE_ERR_INVALID;
+  }
+  a.itU = res->iter_receivers;
+  a.itW = res->iter_weights;
+  a.itV = res->iter_precoders;
   a.gamma = opt->gamma;
   a.gamma_safe = opt->gamma_safe ? 1 : 0;
   a.omega = opt->omega;
@@ -379,8 +392,7 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     int sms2 = 0;
     cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
     const size_t rsz = dims->dtype == AMMMSE_COMPLEX64 ? 4 : 8;
-    const size_t ncol = (size_t)(dims->K / plan.cluster) * dims->d;
-    size_t off = plan.vglob ? (size_t)sms2 * 2 * (size_t)dims->M * ncol * rsz : 0;
+    size_t off = plan.vglob ? (size_t)sms2 * 2 * (size_t)dims->M * vold_ld(dims, plan) * rsz : 0;
     off = (off + 255) & ~(size_t)255;
     a.hplanes = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(workspace) + 256 + off);
   }
@@ -401,6 +413,38 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   else
     ce = cudaLaunchKernel(func, dim3((unsigned)grid), dim3(threads), args, smem, s);
   if (ce != cudaSuccess) return cuda_fail(ce, "kernel launch (solve)");
+  return AMMMSE_OK;
+}
+
+int ammmse_plan_info(const AmmmseDims* dims, const AmmmseOptions* opt, int* info) {
+  int rc = dims_valid(dims);
+  if (rc) return rc;
+  if (!opt || !info) return AMMMSE_ERR_INVALID;
+  Plan p;
+  rc = make_plan(dims, opt->cluster_size, opt->h_placement, opt->tensor_cores, &p);
+  if (rc) return rc;
+  int spec = 0;
+  if (!p.cluster) {
+    for (int i = 0; i < p.e->n_solve_specs; ++i)
+      if (p.e->solve_specs[i].M == dims->M && p.e->solve_specs[i].K == dims->K &&
+          p.e->solve_specs[i].T == p.threads)
+        spec = 1;
+  } else if (!p.tc) {
+    for (int i = 0; i < p.e->n_cluster_specs; ++i) {
+      const ammmse::SpecEntry& sp = p.e->cluster_specs[i];
+      const bool place_ok = sp.sb == 0 || (!p.hres && p.vglob && p.sb == sp.sb);
+      if (sp.M == dims->M && sp.K == dims->K && sp.C == p.cluster && sp.T == p.threads && place_ok)
+        spec = 1;
+    }
+  }
+  info[0] = p.cluster;
+  info[1] = p.hres;
+  info[2] = p.vglob;
+  info[3] = p.sb;
+  info[4] = p.tc;
+  info[5] = (int)p.smem;
+  info[6] = p.threads;
+  info[7] = spec;
   return AMMMSE_OK;
 }
 

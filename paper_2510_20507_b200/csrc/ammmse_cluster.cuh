@@ -22,7 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "ammmse_engine.cuh"
-#include "tc_gemm.cuh"
+#include "tc_stream.cuh"
 
 namespace ammmse {
 
@@ -328,14 +328,25 @@ __device__ __forceinline__ void cgemm_stream2(int P, int Q, int KD, const RC<R>*
 }
 
 constexpr int kStreamStages = 4;
-constexpr int kTcStages = 3;  // cp.async ring depth of the tensor-core GEMM
-constexpr int kTcCols = 256;  // TMEM columns allocated per CTA (tensor-core mode)
+constexpr int kTcStages = 4;  // bulk-copy ring depth of the tensor-core GEMM (tc_stream.cuh)
 
-// tensor-core mode shape rules (UMMA M = 64/128 tiles, N % 16, K steps of 8)
+// tensor-core mode: UMMA tile height for a GEMM with `rows` output rows
+__host__ __device__ inline int tc_tm(int rows) { return rows >= 128 ? 128 : 64; }
+// TMEM columns (power of two >= 32) for accumulators of 8 * ncol columns per tile
+__host__ __device__ inline int tc_tmem_cols(int M, int KN, int ncol) {
+  const int tA = M / tc_tm(M), tB = KN / tc_tm(KN);
+  const int need = 8 * ncol * (tA > tB ? tA : tB);
+  int c = 32;
+  while (c < need) c <<= 1;
+  return c;
+}
+// tensor-core mode shape rules: UMMA M tiles of 64 (single) or 128 rows, N =
+// 4 ncol <= 256 in multiples of 16 (epilogue column blocks), K steps of 8,
+// accumulators within the 512 TMEM columns
 __host__ __device__ inline bool tc_shape_ok(int M, int KN, int ncol) {
-  if (M % 128 || !(KN == 64 || KN % 128 == 0) || ncol % 16 || ncol > 256) return false;
-  const int tA = M / 128, tB = KN >= 128 ? KN / 128 : 1;
-  return 2 * ncol * (tA > tB ? tA : tB) <= kTcCols;
+  auto rows_ok = [](int r) { return r == 64 || (r % 128 == 0 && r > 0); };
+  if (!rows_ok(M) || !rows_ok(KN) || ncol % 16 || 4 * ncol > 256) return false;
+  return tc_tmem_cols(M, KN, ncol) <= 512;
 }
 
 constexpr int kStreamRY = 4, kStreamRX = 2, kStreamTPT = 4;
@@ -351,7 +362,7 @@ struct CLayout {
   int hres;  // 1: H resident in SMEM;  0: H streamed from global through `stage`
   int vglob; // 1: the second V buffer lives in a per-CTA global scratch slot (L2)
   int tc;    // 1: tensor-core GEMMs; the H region holds the tcgen05 operand ring
-  int tc_a, tc_b;  // floats of one ring stage's A / B tile
+  int tc_a, tc_b;  // bytes of one ring stage's A / B tile (tensor-core mode)
   int SB;    // staging buffer size (complex elements) when streamed
   size_t nH, nV, nG;
   size_t oH, oV0, oV1, oG0, oG1, oUall, oPall, oDown;  // R offsets (planar / RC)
@@ -371,16 +382,18 @@ struct CLayout {
     KD = K * DD;
     ncol = KL * DD;
     ldh = ((M + 3) & ~3) + 4;
-    ldv = ncol;
-    ldg = ncol;
+    // tensor-core epilogues walk rows one thread per row: odd row strides keep
+    // those column sweeps free of bank conflicts (the FFMA GEMMs need ncol)
+    ldv = tc_ ? ncol + 1 : ncol;
+    ldg = tc_ ? ncol + 1 : ncol;
     nV = (size_t)M * ldv;
     nG = (size_t)KN * ldg;
     // resident: planar H (2 planes of KN x ldh); streamed: kStreamStages buffers of SB
     // interleaved complex = 2*kStreamStages*SB reals = 2 "planes" of kStreamStages*SB
     nH = hres ? (size_t)KN * ldh : (size_t)kStreamStages * SB;
-    tc_a = 4 * (KN > M ? KN : M) * tcg::KC;
-    tc_b = 4 * ncol * tcg::KC;
-    if (tc) nH = ((size_t)kTcStages * (tc_a + tc_b) + 1) / 2;  // ring floats = 2 nH
+    tc_a = 4 * (KN > M ? KN : M) * tcs::KW * 4;
+    tc_b = 4 * ncol * tcs::KW * 4;
+    if (tc) nH = ((size_t)kTcStages * (tc_a + tc_b) / sizeof(R) + 1) / 2;  // ring reals = 2 nH
     oH = 0;
     oV0 = oH + 2 * nH;
     oV1 = oV0 + 2 * nV;
@@ -399,7 +412,11 @@ struct CLayout {
   // parity: WSR(t) and K1(t+1) run concurrently.
   __host__ __device__ size_t dbl_count() const {
     return (size_t)2 * 2 * K * NN * NN + 2 * 2 * KL * NN * DD + 2 * 2 * KL * DD * DD + 9 * KL +
-           XS_COUNT + 32;
+           XS_COUNT + k1w_count() + 32;
+  }
+  // split-K1 exchange (k1_pipelined; the N = d = 2 closed form does not use it)
+  __host__ __device__ size_t k1w_count() const {
+    return (NN == 2 && DD == 2) ? 0 : (size_t)KL * (2 * DD * DD + NN + 1);
   }
 };
 
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
 
   CLayout<R, NN, DD> L;
   L.init(MC > 0 ? MC : a.M, KC > 0 ? KC : a.K, C, SBC > 0 ? 0 : a.hres, SBC > 0 ? 1 : a.vold_glob,
-         SBC > 0 ? SBC : a.sb_bytes, a.tcm);
+         SBC > 0 ? SBC : a.sb_bytes, TC ? 1 : 0);
   const bool hres = SBC > 0 ? false : a.hres != 0;
   const int M = L.M, K = L.K, KL = L.KL, KN = L.KN, ncol = L.ncol;
   const int ldh = L.ldh, ldv = L.ldv, ldg = L.ldg;
@@ -467,34 +484,41 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   double* ust = dp; dp += KL;
   double* ust2 = dp; dp += KL;
   double* xs = dp; dp += XS_COUNT;
+  double* k1w = dp; dp += L.k1w_count();  // split-K1 exchange
   double* red = dp;
 
-  // ---- tensor-core mode: TMEM accumulator, per-stage mbarriers ----
-  __shared__ uint64_t tc_mbar[kTcStages];
-  __shared__ uint32_t tc_uses[kTcStages];
+  // ---- tensor-core mode: bulk-copy ring with full / done mbarriers, TMEM accumulators ----
+  __shared__ uint64_t tc_full[kTcStages], tc_bready[kTcStages], tc_done[kTcStages], tc_fin;
   __shared__ uint32_t tc_tmem_slot;
-  tcg::Ring ring;
-  ring.stage = reinterpret_cast<float*>(base + L.oH);
-  ring.a_floats = L.tc_a;
-  ring.b_floats = L.tc_b;
-  ring.mbar = tc_mbar;
-  ring.uses = tc_uses;
-  ring.tmem = 0;
+  tcs::Pipe pipe;
+  pipe.ring = reinterpret_cast<unsigned char*>(base + L.oH);
+  pipe.S = kTcStages;
+  pipe.a_bytes = L.tc_a;
+  pipe.stage_bytes = L.tc_a + L.tc_b;
+  pipe.full = tc_full;
+  pipe.bready = tc_bready;
+  pipe.done = tc_done;
+  pipe.fin = &tc_fin;
+  pipe.tmem = 0;
+  tcs::Seq tc_seq;             // pipeline position (identical in every thread)
   const float* hpB = nullptr;  // pre-split H planes (rows r, K = m), this cluster's slot
   const float* hpA = nullptr;  // pre-split H^T planes (rows m, K = r)
-  if (TC && L.tc) {
+  const int tmA = tc_tm(M), tmB = tc_tm(KN);
+  if constexpr (TC) {
     if (tid == 0) {
       for (int q = 0; q < kTcStages; ++q) {
-        umma::mbar_init(&tc_mbar[q], 1);
-        tc_uses[q] = 0;
+        umma::mbar_init(&tc_full[q], 1);
+        umma::mbar_init(&tc_bready[q], 1);  // the producing warp (tcs::gemm)
+        umma::mbar_init(&tc_done[q], 1);
       }
+      umma::mbar_init(&tc_fin, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if ((tid >> 5) == 0) umma::tmem_alloc<kTcCols>(&tc_tmem_slot);
+    if ((tid >> 5) == 0) umma::tmem_alloc<512>(&tc_tmem_slot);  // one CTA per SM
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    ring.tmem = tc_tmem_slot;
+    pipe.tmem = tc_tmem_slot;
     const size_t hp = (size_t)8 * L.KN * L.M;
     float* slot = a.hplanes + (size_t)(blockIdx.x / C) * hp;
     hpB = slot;
@@ -518,63 +542,139 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   auto gram_partials = [&](const R* Xr, const R* Xi, int buf) {
     user_grams<R, NN>(Xr, Xi, ldg, ncol, K, gx[buf]);
   };
-  // reduced Gram of own user kl (fixed rank order)
+  // cluster sum of the own users' Gram partials, all threads in parallel (the
+  // remote DSMEM loads are independent; fixed rank order), written back over
+  // this CTA's own-user slots of gx[buf]: only this CTA reads those slots
+  // (every CTA sums the slots of ITS users), and each element is read and
+  // rewritten by one thread.  Called after the cluster barrier that publishes
+  // gx[buf]; the partials are not rewritten before the next cluster barrier.
+  auto gram_reduce = [&](int buf) {
+    constexpr int per = NN * NN;
+    for (int i = tid; i < KL * per; i += blockDim.x) {
+      const size_t gi = (size_t)k0 * per + i;
+      cd s = cl.map_shared_rank(gx[buf], 0)[gi];
+      for (int c = 1; c < C; ++c) s = cadd(s, cl.map_shared_rank(gx[buf], c)[gi]);
+      gx[buf][gi] = s;
+    }
+  };
+  // reduced Gram of own user kl (after gram_reduce(buf) and a block barrier)
   auto gram_of = [&](int buf, int kl, cd (&Tg)[NN][NN]) {
-    const int k = k0 + kl;
+    const cd* g = gx[buf] + (size_t)(k0 + kl) * NN * NN;
 #pragma unroll
     for (int p = 0; p < NN; ++p)
 #pragma unroll
-      for (int q = 0; q < NN; ++q) Tg[p][q] = cmk(0.0);
-    for (int c = 0; c < C; ++c) {
-      const cd* g = cl.map_shared_rank(gx[buf], c) + (size_t)k * NN * NN;
-#pragma unroll
-      for (int p = 0; p < NN; ++p)
-#pragma unroll
-        for (int q = 0; q < NN; ++q) Tg[p][q] = cadd(Tg[p][q], g[p * NN + q]);
-    }
+      for (int q = 0; q < NN; ++q) Tg[p][q] = g[p * NN + q];
   };
   // per-user K1 of own users kl = first, first + step, ... from the reduced
   // Gram gx[0] and the work Ĝ in G[gsrc]; W_prev / ln det W_prev from bank
   // bin, U / W / ln det W to bank bout (solvers.py:210-254)
-  auto k1_users = [&](int gsrc, bool weighted, bool want_f, int bin, int bout, int first,
-                      int step) {
-    const cd* wprev = wcb[bin];
+  auto k1_load = [&](int gsrc, int kl, cd (&Tg)[NN][NN], cd (&Gkk)[NN][DD]) {
+    gram_of(0, kl, Tg);
+#pragma unroll
+    for (int p = 0; p < NN; ++p)
+#pragma unroll
+      for (int s = 0; s < DD; ++s) {
+        const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
+        Gkk[p][s] = cmk((double)Gr[gsrc][idx], (double)Gi[gsrc][idx]);
+      }
+  };
+  auto k1_wprev = [&](int bin, int kl, cd (&Wp)[DD][DD]) {
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) Wp[p][q] = wcb[bin][(kl * DD + p) * DD + q];
+  };
+  auto k1_store = [&](int kl, const K1Out<NN, DD>& o, int bout) {
     cd* ucache = ucb[bout];
     cd* wcache = wcb[bout];
+#pragma unroll
+    for (int p = 0; p < NN; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) {
+        const int ig = ((k0 + kl) * NN + p) * DD + q, il = (kl * NN + p) * DD + q;
+        Uall[ig] = RC<R>{(R)o.U[p][q].r, (R)o.U[p][q].i};
+        Pall[ig] = RC<R>{(R)o.P[p][q].r, (R)o.P[p][q].i};
+        Down[il] = RC<R>{(R)o.D[p][q].r, (R)o.D[p][q].i};
+        ucache[il] = o.U[p][q];
+      }
+#pragma unroll
+    for (int p = 0; p < DD; ++p)
+#pragma unroll
+      for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = o.W[p][q];
+    lndb[bout][kl] = o.lndetw;
+    fu[kl] = o.fu;
+    fw[kl] = o.fw;
+    ust[kl] = o.status;
+  };
+  auto k1_users = [&](int gsrc, bool weighted, bool want_f, int bin, int bout, int first,
+                      int step) {
     for (int kl = first; kl < KL; kl += step) {
       cd Tg[NN][NN], Gkk[NN][DD], Wp[DD][DD];
-      gram_of(0, kl, Tg);
-#pragma unroll
-      for (int p = 0; p < NN; ++p)
-#pragma unroll
-        for (int s = 0; s < DD; ++s) {
-          const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
-          Gkk[p][s] = cmk((double)Gr[gsrc][idx], (double)Gi[gsrc][idx]);
-        }
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) Wp[p][q] = wprev[(kl * DD + p) * DD + q];
+      k1_load(gsrc, kl, Tg, Gkk);
+      k1_wprev(bin, kl, Wp);
       K1Out<NN, DD> o;
       k1_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], Wp, lndb[bin][kl], weighted, want_f, o);
-#pragma unroll
-      for (int p = 0; p < NN; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) {
-          const int ig = ((k0 + kl) * NN + p) * DD + q, il = (kl * NN + p) * DD + q;
-          Uall[ig] = RC<R>{(R)o.U[p][q].r, (R)o.U[p][q].i};
-          Pall[ig] = RC<R>{(R)o.P[p][q].r, (R)o.P[p][q].i};
-          Down[il] = RC<R>{(R)o.D[p][q].r, (R)o.D[p][q].i};
-          ucache[il] = o.U[p][q];
+      k1_store(kl, o, bout);
+    }
+  };
+  // K1(t+1) of the pipelined loop, run by threads 32.. (warp 0 is on WSR(t)).
+  // Generic N, d in the weighted stage: the receiver half (k1_part_u) on warp 1
+  // and the Woodbury weight half (k1_part_w) on warp 2 run concurrently, one
+  // lane per user, then warp 1 combines (same arithmetic as k1_math, so the
+  // results are identical to the one-thread path).
+  auto k1_pipelined = [&](int gsrc, bool weighted, int bin, int bout) {
+    constexpr bool closed = NN == 2 && DD == 2;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (closed || !weighted || KL > 32 || blockDim.x < 96) {
+      if (tid >= 32) k1_users(gsrc, weighted, true, bin, bout, tid - 32, blockDim.x - 32);
+      return;
+    }
+    if constexpr (!closed) {
+      constexpr int wstride = 2 * DD * DD + NN + 1;  // doubles per user in k1w
+      if (warp == 1) {
+        K1U<NN, DD> u;
+        cd Tg[NN][NN], Gkk[NN][DD];
+        if (lane < KL) {
+          cd Wp[DD][DD];
+          k1_load(gsrc, lane, Tg, Gkk);
+          k1_wprev(bin, lane, Wp);
+          k1_part_u<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[lane], Wp, lndb[bin][lane], true, u);
         }
+        asm volatile("bar.sync 1, 64;\n" ::: "memory");
+        if (lane < KL) {
+          const double* w = k1w + (size_t)lane * wstride;
+          cd Wm[DD][DD];
+          double pv[NN];
 #pragma unroll
-      for (int p = 0; p < DD; ++p)
+          for (int p = 0; p < DD; ++p)
 #pragma unroll
-        for (int q = 0; q < DD; ++q) wcache[(kl * DD + p) * DD + q] = o.W[p][q];
-      lndb[bout][kl] = o.lndetw;
-      fu[kl] = o.fu;
-      fw[kl] = o.fw;
-      ust[kl] = o.status;
+            for (int q = 0; q < DD; ++q) Wm[p][q] = cmk(w[2 * (p * DD + q)], w[2 * (p * DD + q) + 1]);
+#pragma unroll
+          for (int a = 0; a < NN; ++a) pv[a] = w[2 * DD * DD + a];
+          K1Out<NN, DD> o;
+          k1_combine<NN, DD>(u, Wm, pv, (int)w[2 * DD * DD + NN], alpha[lane], true, true, o);
+          k1_store(lane, o, bout);
+        }
+      } else if (warp == 2) {
+        if (lane < KL) {
+          cd Tg[NN][NN], Gkk[NN][DD];
+          k1_load(gsrc, lane, Tg, Gkk);
+          K1W<NN, DD> wv;
+          k1_part_w<NN, DD>(Tg, Gkk, ctl.sigma2, wv);
+          double* w = k1w + (size_t)lane * wstride;
+#pragma unroll
+          for (int p = 0; p < DD; ++p)
+#pragma unroll
+            for (int q = 0; q < DD; ++q) {
+              w[2 * (p * DD + q)] = wv.W[p][q].r;
+              w[2 * (p * DD + q) + 1] = wv.W[p][q].i;
+            }
+#pragma unroll
+          for (int a = 0; a < NN; ++a) w[2 * DD * DD + a] = wv.piv[a];
+          w[2 * DD * DD + NN] = (double)wv.pd;
+        }
+        asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      }
     }
   };
   // per-CTA K1 sums -> exchange slots (one thread, after the K1 writes are visible)
@@ -669,8 +769,10 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   // the SMEM slot 0 (vc = vx = 0, vo = 1, save): GEMM-B always reads SMEM.
   auto grad_step = [&](int ysrc, int vc, int vo, int vx, bool save, double step, double omega,
                        bool extrap) {
-    const R* vcr = Vr[vc];
+    const R* vcr = Vr[vc];  // always shared memory (V_old is the only global slot)
     const R* vci = Vi[vc];
+    AMMMSE_SHARED(vcr);
+    AMMMSE_SHARED(vci);
     R* vor = Vr[vo];
     R* voi = Vi[vo];
     R* xr = Vr[vx];
@@ -679,11 +781,14 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     double pw = 0.0;
     // V_old in global scratch (h_placement 3): staged into the free H ring
     // after the K loop, so the epilogue reads it from shared memory
-    const bool stage_vold = extrap && L.vglob && vo == 1 && !hres &&
-                            L.nV <= (size_t)kStreamStages * L.SB &&
+    const size_t ring_reals = TC ? 2 * L.nH : (size_t)2 * kStreamStages * L.SB;
+    const bool stage_vold = extrap && L.vglob && vo == 1 && !hres && 2 * L.nV <= ring_reals &&
                             (2 * L.nV * sizeof(R)) % 16 == 0;
     const R* rdr = stage_vold ? reinterpret_cast<const R*>(stage) : vor;
     const R* rdi = stage_vold ? rdr + L.nV : voi;
+    // tensor-core epilogues run one thread per row p: the global V_old slot is
+    // then column-major (q * M + p) so the per-row saves coalesce
+    const bool vo_cm = TC && L.vglob && vo == 1;
     auto pre = [&]() {
       if (stage_vold) {
         const int n16 = (int)((2 * L.nV * sizeof(R)) / 16);
@@ -697,42 +802,28 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     };
     auto epi = [&](int p, int q, R gr, R gi) {
       const int o = p * ldv + q;
+      const int ov = vo_cm ? q * M + p : o;
       const R cr0 = vcr[o], ci0 = vci[o];
       R vr = cr0, vi = ci0;
       if (extrap) {
-        vr = vr + om * (vr - rdr[o]);
-        vi = vi + om * (vi - rdi[o]);
+        vr = vr + om * (vr - rdr[ov]);
+        vi = vi + om * (vi - rdi[ov]);
       }
       const R x_r = vr - st * gr, x_i = vi - st * gi;
       if (save) {
-        vor[o] = cr0;
-        voi[o] = ci0;
+        vor[ov] = cr0;
+        voi[ov] = ci0;
       }
       xr[o] = x_r;
       xi[o] = x_i;
       pw += (double)x_r * (double)x_r + (double)x_i * (double)x_i;
     };
-    if constexpr (sizeof(R) == 4) {
-      if (TC && L.tc) {  // ∇' = H^H Ŷ on tcgen05 (signs +,-), epilogue per (row, col, part)
-        tcg::gemm<kTcStages>(ring, M, ncol, KN, hpA, (const float*)Gr[ysrc],
-                             (const float*)Gi[ysrc], ldg, 1.f, -1.f);
-        tcg::for_each_d(ring, M, ncol, [&](int p, int q, int part, float g) {
-          const int o = p * ldv + q;
-          const R* vcp = part ? vci : vcr;
-          R* vop = part ? voi : vor;
-          R* x = part ? xi : xr;
-          const R c0 = vcp[o];
-          R v = c0;
-          if (extrap) v = v + om * (v - vop[o]);
-          const R xv = v - st * g;
-          if (save) vop[o] = c0;
-          x[o] = xv;
-          pw += (double)xv * (double)xv;
-        });
-        umma::fence_before();
-      }
-    }
-    if (TC && L.tc) {
+    if constexpr (TC) {  // ∇' = H^H Ŷ on tcgen05 (conj A), epilogue one thread per row
+      tcs::gemm(pipe, tc_seq, hpA, tmA, M / tmA, KN, ncol, (const float*)Gr[ysrc],
+                (const float*)Gi[ysrc], ldg);
+      pre();
+      tcs::for_each(pipe, tmA, M / tmA, ncol, true,
+                    [&](int p, int q, float gr, float gi) { epi(p, q, (R)gr, (R)gi); });
     } else if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
     else if ((M / 4) * (ncol / 4) < (int)blockDim.x &&
@@ -762,31 +853,24 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
     R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
     const R om = (R)omega;
+    AMMMSE_SHARED(gr);
+    AMMMSE_SHARED(gi);
     auto epi = [&](int p, int q, R cr, R ci) {
       const int o = p * ldg + q;
       gr[o] = cr;
       gi[o] = ci;
       if (hr) {  // ω = 0: plain copy (G_prev may be uninitialised shared memory)
+        AMMMSE_SHARED(hr);
+        AMMMSE_SHARED(hi);
         hr[o] = om == R(0) ? cr : cr + om * (cr - hr[o]);
         hi[o] = om == R(0) ? ci : ci + om * (ci - hi[o]);
       }
     };
-    if constexpr (sizeof(R) == 4) {
-      if (TC && L.tc) {  // G = H V on tcgen05 (signs -,+)
-        tcg::gemm<kTcStages>(ring, KN, ncol, M, hpB, (const float*)Vr[src], (const float*)Vi[src],
-                             ldv, -1.f, 1.f);
-        tcg::for_each_d(ring, KN, ncol, [&](int p, int q, int part, float g) {
-          const int o = p * ldg + q;
-          (part ? gi : gr)[o] = g;
-          if (hr) {
-            R* h = part ? hi : hr;
-            h[o] = om == R(0) ? g : g + om * (g - h[o]);
-          }
-        });
-        umma::fence_before();
-      }
-    }
-    if (TC && L.tc) {
+    if constexpr (TC) {  // G = H V on tcgen05, epilogue one thread per row
+      tcs::gemm(pipe, tc_seq, hpB, tmB, KN / tmB, M, ncol, (const float*)Vr[src],
+                (const float*)Vi[src], ldv);
+      tcs::for_each(pipe, tmB, KN / tmB, ncol, false,
+                    [&](int p, int q, float cr, float ci) { epi(p, q, (R)cr, (R)ci); });
     } else if (hres)
       cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);
     else if (stream2_ok<R, 2, 4, false>(KN, ncol, M, ldv, L.SB, blockDim.x))
@@ -815,12 +899,13 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       const RC<R>* Hg = reinterpret_cast<const RC<R>*>(a.H) + (size_t)r * KN * M;
       Hcur = Hg;
       if constexpr (sizeof(R) == 4) {
-        if (TC && L.tc) {  // this CTA's share of the pre-split H / H^T planes (rows r0..r1)
+        if (TC) {  // this CTA's share of the pre-split H / H^T planes (rows r0..r1)
           const int r0 = crank * (KN / C), r1 = (crank + 1) * (KN / C);
           const float2* H2 = reinterpret_cast<const float2*>(Hg);
-          tcg::split_planes(H2, KN, M, false, const_cast<float*>(hpB), r0, r1);
-          tcg::split_planes(H2, KN, M, true, const_cast<float*>(hpA), r0, r1);
-          __threadfence();  // visible to the other CTAs' cp.async before the next cluster barrier
+          tcs::split_h(H2, KN, M, false, const_cast<float*>(hpB), r0, r1);
+          tcs::split_h(H2, KN, M, true, const_cast<float*>(hpA), r0, r1);
+          umma::fence_proxy_async_global();  // generic writes -> the cluster's bulk copies
+          __threadfence();  // visible to the other CTAs before the next cluster barrier
         }
       }
       if (hres) {
@@ -934,6 +1019,8 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     bool wn = stage_flag();  // the flag K1(t) was computed with
     gram_partials(Gr[1], Gi[1], 0);
     cl.sync();
+    gram_reduce(0);
+    __syncthreads();
     k1_phase(1, wn, true, 0, 1);
     pc.mark(9);  // setup: load, bounds, G = H V0, K1(1)
 
@@ -976,7 +1063,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
       if (scale != 1.0) {
         const R sc = (R)scale;
-        for (int i = tid; i < M * ncol; i += blockDim.x) {
+        for (int i = tid; i < M * ldv; i += blockDim.x) {  // (padding columns too)
           Vr[vx][i] *= sc;
           Vi[vx][i] *= sc;
         }
@@ -997,6 +1084,9 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       // speculated stage flag of t+1 (thread 0 updates ctl.latched below)
       const bool wn_spec = ctl.latched || wn;
       cl.sync();
+      gram_reduce(1);
+      if (more) gram_reduce(0);
+      __syncthreads();
       pc.mark(4);
       if (tid < 32) {  // warp 0: rates / f_after_v of own users (lanes), CTA partials
         const int lane = tid;
@@ -1041,12 +1131,32 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
           xs[XS_ST2] = f2 < KL ? ust2[f2] : 0.0;
         }
       } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
-        k1_users(cur, wn_spec, true, bk, bk ^ 1, tid - 32, blockDim.x - 32);
+        k1_pipelined(cur, wn_spec, bk, bk ^ 1);
       }
       __syncthreads();
       if (more && tid == 32) k1_publish();
       cl.sync();
       pc.mark(5);
+      if (a.itU) {  // block iterate of t (solvers.py:487-488), own users / columns
+        const size_t it = (size_t)r * a.max_iters + (t - 1);
+        double* dU = a.itU + (it * K + k0) * (size_t)NN * DD * 2;
+        double* dW = a.itW + (it * K + k0) * (size_t)DD * DD * 2;
+        double* dV = a.itV + (it * K + k0) * (size_t)M * DD * 2;
+        for (int i = tid; i < KL * NN * DD; i += blockDim.x) {
+          dU[2 * i] = ucb[bk][i].r;
+          dU[2 * i + 1] = ucb[bk][i].i;
+        }
+        for (int i = tid; i < KL * DD * DD; i += blockDim.x) {
+          dW[2 * i] = wcb[bk][i].r;
+          dW[2 * i + 1] = wcb[bk][i].i;
+        }
+        for (int i = tid; i < KL * M * DD; i += blockDim.x) {
+          const int kl = i / (M * DD), rem = i - kl * M * DD, m = rem / DD, s = rem - m * DD;
+          const int o = m * ldv + kl * DD + s;
+          dV[2 * i] = (double)Vr[vx][o];
+          dV[2 * i + 1] = (double)Vi[vx][o];
+        }
+      }
       if (tid == 0) {  // state machine of iteration t, identical in every CTA
         if (!ctl.latched && wn) {
           if (a.latch) ctl.latched = 1;
@@ -1119,13 +1229,15 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     if (ctl.status == 0) {
       const int cur = ctl.cur, oth = 1 - cur;
       const bool weighted = ctl.latched || ctl.last_weighted;
-      for (int i = tid; i < KN * ncol; i += blockDim.x) {
+      for (int i = tid; i < KN * ldg; i += blockDim.x) {
         Gr[oth][i] = Gr[cur][i];
         Gi[oth][i] = Gi[cur][i];
       }
       __syncthreads();
       gram_partials(Gr[oth], Gi[oth], 0);
       cl.sync();
+      gram_reduce(0);
+      __syncthreads();
       k1_phase(oth, weighted, false, 0, 0);
       int st = xfirst(XS_ST1);
       __syncthreads();
@@ -1137,7 +1249,8 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
         double scale = 1.0;
         if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);
         double dsum = 0.0, vsum = 0.0;
-        for (int i = tid; i < M * ncol; i += blockDim.x) {
+        for (int i = tid; i < M * ldv; i += blockDim.x) {
+          if (i % ldv >= ncol) continue;  // padding column (tensor-core layout)
           const double a_r = (double)Vr[rc][i], a_i = (double)Vi[rc][i];
           const double dr = a_r - (double)((R)(Vr[rx][i] * (R)scale));
           const double di = a_i - (double)((R)(Vi[rx][i] * (R)scale));
@@ -1183,9 +1296,9 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     pc.mark(8);
   }
   pc.flush();
-  if (TC && L.tc) {
+  if constexpr (TC) {
     __syncthreads();
-    if ((tid >> 5) == 0) umma::tmem_dealloc<kTcCols>(ring.tmem);
+    if ((tid >> 5) == 0) umma::tmem_dealloc<512>(pipe.tmem);
   }
 }
 

@@ -71,6 +71,9 @@ struct EngineArgs {
   int* status;
   double* gamma_used;
   double* trace;
+  double* itU;  // recorded iterates (optional): (B, T, K, N, d), (B, T, K, d, d),
+  double* itW;  // (B, T, K, M, d) complex128
+  double* itV;
   double gamma;
   double omega, eps1, eps2;
   int gamma_safe;
@@ -484,50 +487,56 @@ __device__ __forceinline__ void cgemm_any(int P, int Q, int KD, const R* Ar, con
                                });
 }
 
-// Per-user Grams  gram[k] = sum_{j < ncols} X[kN+a][j] conj(X[kN+b][j])  (fp64),
-// one warp per user, lanes over columns, full Hermitian N x N stored.
+// Gram of user k over `ncols` columns of X, computed by one warp (lanes over
+// columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
 template <typename R, int NN>
-__device__ __forceinline__ void user_grams(const R* __restrict__ Xr, const R* __restrict__ Xi,
-                                           int ld, int ncols, int K, cd* __restrict__ gram) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = warp; k < K; k += nw) {
-    double sr[NN][NN], si[NN][NN];
+__device__ __forceinline__ void gram_warp(int k, const R* __restrict__ Xr, const R* __restrict__ Xi,
+                                         int ld, int ncols, int lane, cd* __restrict__ gram) {
+  double sr[NN][NN], si[NN][NN];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
+  for (int j = lane; j < ncols; j += 32) {
+    double gr[NN], gi[NN];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      gr[a] = (double)Xr[(k * NN + a) * ld + j];
+      gi[a] = (double)Xi[(k * NN + a) * ld + j];
+    }
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
-      for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
-    for (int j = lane; j < ncols; j += 32) {
-      double gr[NN], gi[NN];
-#pragma unroll
-      for (int a = 0; a < NN; ++a) {
-        gr[a] = (double)Xr[(k * NN + a) * ld + j];
-        gi[a] = (double)Xi[(k * NN + a) * ld + j];
+      for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
+        sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
+        if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
       }
+  }
 #pragma unroll
-      for (int a = 0; a < NN; ++a)
+  for (int a = 0; a < NN; ++a)
 #pragma unroll
-        for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
-          sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
-          if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
-        }
+    for (int b = 0; b <= a; ++b) {
+      sr[a][b] = warp_allsum(sr[a][b]);
+      if (b < a) si[a][b] = warp_allsum(si[a][b]);
     }
+  if (lane == 0) {
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
       for (int b = 0; b <= a; ++b) {
-        sr[a][b] = warp_allsum(sr[a][b]);
-        if (b < a) si[a][b] = warp_allsum(si[a][b]);
+        gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
+        if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
       }
-    if (lane == 0) {
-#pragma unroll
-      for (int a = 0; a < NN; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b) {
-          gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
-          if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
-        }
-    }
   }
+}
+
+// Per-user Grams  gram[k] = sum_{j < ncols} X[kN+a][j] conj(X[kN+b][j])  (fp64),
+// one warp per user (gram_warp), full Hermitian N x N stored.
+template <typename R, int NN>
+__device__ __forceinline__ void user_grams(const R* __restrict__ Xr, const R* __restrict__ Xi,
+                                           int ld, int ncols, int K, cd* __restrict__ gram) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < K; k += nw) gram_warp<R, NN>(k, Xr, Xi, ld, ncols, lane, gram);
 }
 
 // Warp reduce-scatter of P (power of two <= 32) fp64 values: halving levels
@@ -655,49 +664,6 @@ __device__ __forceinline__ void gram_pair(int k, const R* X0r, const R* X0i, cd*
       gram_store<NN>(k, idx, tot, gram0);
     else if (idx < 2 * V && X1r)
       gram_store<NN>(k, idx - V, tot, gram1);
-  }
-}
-
-// Gram of user k over `ncols` columns of X, computed by one warp (lanes over
-// columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
-template <typename R, int NN>
-__device__ __forceinline__ void gram_one(int k, const R* __restrict__ Xr, const R* __restrict__ Xi,
-                                         int ld, int ncols, int lane, cd* __restrict__ gram) {
-  double sr[NN][NN], si[NN][NN];
-#pragma unroll
-  for (int a = 0; a < NN; ++a)
-#pragma unroll
-    for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
-  for (int j = lane; j < ncols; j += 32) {
-    double gr[NN], gi[NN];
-#pragma unroll
-    for (int a = 0; a < NN; ++a) {
-      gr[a] = (double)Xr[(k * NN + a) * ld + j];
-      gi[a] = (double)Xi[(k * NN + a) * ld + j];
-    }
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b) {  // g_a * conj(g_b)
-        sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
-        if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
-      }
-  }
-#pragma unroll
-  for (int a = 0; a < NN; ++a)
-#pragma unroll
-    for (int b = 0; b <= a; ++b) {
-      sr[a][b] = warp_allsum(sr[a][b]);
-      if (b < a) si[a][b] = warp_allsum(si[a][b]);
-    }
-  if (lane == 0) {
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b) {
-        gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
-        if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
-      }
   }
 }
 
@@ -864,102 +830,13 @@ struct Engine {
     ust2[k] = st;
   }
 
-  // Gram of user k over `ncols` columns of X, computed by one warp (lanes over
-  // columns, fp64, fixed shuffle tree); lane 0 stores the Hermitian N x N.
+  // Gram of user k over `ncols` columns of X (one warp, gram_warp)
   __device__ void gram_user(int k, const R* __restrict__ Xr, const R* __restrict__ Xi, int ld,
                             int ncols, int lane, cd* gram) {
     AMMMSE_SHARED(Xr);
     AMMMSE_SHARED(Xi);
     AMMMSE_SHARED(gram);
-    double sr[NN][NN], si[NN][NN];
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b < NN; ++b) sr[a][b] = si[a][b] = 0.0;
-    for (int j = lane; j < ncols; j += 32) {
-      double gr[NN], gi[NN];
-#pragma unroll
-      for (int a = 0; a < NN; ++a) {
-        gr[a] = (double)Xr[(k * NN + a) * ld + j];
-        gi[a] = (double)Xi[(k * NN + a) * ld + j];
-      }
-#pragma unroll
-      for (int a = 0; a < NN; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b) {
-          sr[a][b] = fma(gr[a], gr[b], fma(gi[a], gi[b], sr[a][b]));
-          if (b < a) si[a][b] = fma(gi[a], gr[b], fma(-gr[a], gi[b], si[a][b]));
-        }
-    }
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
-#pragma unroll
-      for (int b = 0; b <= a; ++b) {
-        sr[a][b] = warp_allsum(sr[a][b]);
-        if (b < a) si[a][b] = warp_allsum(si[a][b]);
-      }
-    if (lane == 0) {
-#pragma unroll
-      for (int a = 0; a < NN; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b) {
-          gram[(k * NN + a) * NN + b] = cmk(sr[a][b], b < a ? si[a][b] : 0.0);
-          if (b < a) gram[(k * NN + b) * NN + a] = cmk(sr[a][b], -si[a][b]);
-        }
-    }
-  }
-
-  // Ŷ row block of user m (rows mN..mN+N-1), in place over the work G, lanes
-  // over columns.
-  __device__ void yhat_user(int m, R* Gwr, R* Gwi, int ldg, int KD, int lane) {
-    for (int j = lane; j < KD; j += 32) {
-      const int b = j / DD, s = j - b * DD;
-      R yr[NN], yi[NN];
-      if (b == m) {
-#pragma unroll
-        for (int a = 0; a < NN; ++a) {
-          const RC<R> v = Df[(m * NN + a) * DD + s];
-          yr[a] = v.r;
-          yi[a] = v.i;
-        }
-      } else {
-        R gr[NN], gi[NN], qr[DD], qi[DD];
-#pragma unroll
-        for (int a = 0; a < NN; ++a) {
-          gr[a] = Gwr[(m * NN + a) * ldg + j];
-          gi[a] = Gwi[(m * NN + a) * ldg + j];
-        }
-#pragma unroll
-        for (int p = 0; p < DD; ++p) {  // q = U_m^H g
-          R sr = 0, si = 0;
-#pragma unroll
-          for (int a = 0; a < NN; ++a) {
-            const RC<R> u = Uf[(m * NN + a) * DD + p];
-            sr = fma(u.r, gr[a], fma(u.i, gi[a], sr));
-            si = fma(u.r, gi[a], fma(-u.i, gr[a], si));
-          }
-          qr[p] = sr;
-          qi[p] = si;
-        }
-#pragma unroll
-        for (int a = 0; a < NN; ++a) {  // y = P_m q
-          R sr = 0, si = 0;
-#pragma unroll
-          for (int p = 0; p < DD; ++p) {
-            const RC<R> pp = Pf[(m * NN + a) * DD + p];
-            sr = fma(pp.r, qr[p], fma(-pp.i, qi[p], sr));
-            si = fma(pp.r, qi[p], fma(pp.i, qr[p], si));
-          }
-          yr[a] = sr;
-          yi[a] = si;
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < NN; ++a) {
-        Gwr[(m * NN + a) * ldg + j] = yr[a];
-        Gwi[(m * NN + a) * ldg + j] = yi[a];
-      }
-    }
+    gram_warp<R, NN>(k, Xr, Xi, ld, ncols, lane, gram);
   }
 
   // Gram(Ĝ) on all warps | receiver / weight / gradient factors with lanes =
@@ -1443,6 +1320,27 @@ __global__ void __launch_bounds__(kMaxThreads, (NN * DD <= 4) ? MB : 1) ammmse_s
         __syncthreads();
       }
       pc.mark(4);
+      if (a.itU) {  // block iterate of t (solvers.py:487-488): U(t), W(t), V_new(t) = scale X
+        const size_t it = (size_t)r * a.max_iters + (t - 1);
+        double* dU = a.itU + it * (size_t)K * NN * DD * 2;
+        double* dW = a.itW + it * (size_t)K * DD * DD * 2;
+        double* dV = a.itV + it * (size_t)K * M * DD * 2;
+        for (int i = tid; i < K * NN * DD; i += blockDim.x) {
+          dU[2 * i] = e.ucb[bk][i].r;
+          dU[2 * i + 1] = e.ucb[bk][i].i;
+        }
+        for (int i = tid; i < K * DD * DD; i += blockDim.x) {
+          dW[2 * i] = e.wcb[bk][i].r;
+          dW[2 * i + 1] = e.wcb[bk][i].i;
+        }
+        const R sc = (R)scale;
+        for (int i = tid; i < K * M * DD; i += blockDim.x) {
+          const int k = i / (M * DD), rem = i - k * M * DD, m = rem / DD, s = rem - m * DD;
+          const int o = m * ldv + k * DD + s;
+          dV[2 * i] = (double)(sc * e.Vr[oth][o]);
+          dV[2 * i + 1] = (double)(sc * e.Vi[oth][o]);
+        }
+      }
       if (tid < 32) {  // warp 0: rates (lanes = users), reductions, state machine
         const int lane = tid;
         for (int k = lane; k < K; k += 32) e.wsr_user(k, e.Gr[oth], e.Gi[oth], ldg, ctl.sigma2, bk);

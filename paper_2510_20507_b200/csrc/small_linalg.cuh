@@ -4,9 +4,8 @@
 // These are the device restatements of the reference's L0 helpers
 // (pkg/src/wsrbeam/linalg.py): hermitianize (:12-14), solve_hpd via a lower
 // Cholesky factor (:17-24, scipy cho_factor/cho_solve = LAPACK zpotrf/zpotrs),
-// lndet_hpd from the Cholesky diagonal (:27-30); plus the general d x d solve
-// numpy.linalg.solve does at solvers.py:248 (LU with partial pivoting) and the
-// eigvalsh used by compute_bounds (objective.py:231).
+// lndet_hpd from the Cholesky diagonal (:27-30); plus the eigvalsh used by
+// compute_bounds (objective.py:231).
 #pragma once
 #include <math.h>
 
@@ -117,53 +116,6 @@ __device__ __forceinline__ void chol_solve(const cd (&L)[n][n], cd (&B)[n][m]) {
       B[i][c] = cscale(t, 1.0 / L[i][i].r);
     }
   }
-}
-
-// General inverse by Gauss-Jordan elimination with partial pivoting
-// (numpy.linalg.solve(T, I) at solvers.py:248 is LU with partial pivoting).
-// Returns false for an exactly singular or non-finite matrix.
-template <int n>
-__device__ __forceinline__ bool inverse_gj(cd (&A)[n][n], cd (&X)[n][n]) {
-#pragma unroll
-  for (int i = 0; i < n; ++i)
-#pragma unroll
-    for (int j = 0; j < n; ++j) X[i][j] = cmk(i == j ? 1.0 : 0.0);
-#pragma unroll
-  for (int c = 0; c < n; ++c) {
-    // pivot search on column c, rows c..n-1 (register-resident: swap by select)
-    int piv = c;
-    double best = cabs2(A[c][c]);
-#pragma unroll
-    for (int r = c + 1; r < n; ++r) {
-      const double v = cabs2(A[r][c]);
-      if (v > best) { best = v; piv = r; }
-    }
-    if (!(best > 0.0) || !isfinite(best)) return false;
-#pragma unroll
-    for (int r = c + 1; r < n; ++r) {
-      if (r == piv) {
-#pragma unroll
-        for (int j = 0; j < n; ++j) {
-          cd t = A[c][j]; A[c][j] = A[r][j]; A[r][j] = t;
-          t = X[c][j]; X[c][j] = X[r][j]; X[r][j] = t;
-        }
-      }
-    }
-    const cd inv = cdiv(cmk(1.0), A[c][c]);
-#pragma unroll
-    for (int j = 0; j < n; ++j) { A[c][j] = cmul(A[c][j], inv); X[c][j] = cmul(X[c][j], inv); }
-#pragma unroll
-    for (int r = 0; r < n; ++r) {
-      if (r == c) continue;
-      const cd f = A[r][c];
-#pragma unroll
-      for (int j = 0; j < n; ++j) {
-        A[r][j] = csub(A[r][j], cmul(f, A[c][j]));
-        X[r][j] = csub(X[r][j], cmul(f, X[c][j]));
-      }
-    }
-  }
-  return true;
 }
 
 // Largest eigenvalue of a Hermitian n x n matrix (full storage), via cyclic

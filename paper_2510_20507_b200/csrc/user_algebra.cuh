@@ -205,38 +205,72 @@ __device__ __forceinline__ void wsr_math_22(const cd (&Tg)[2][2], const cd (&G)[
   }
 }
 
-// weighted: W update (else W = I).  want_f: compute f_after_u / f_after_w
-// terms (the exit residual pass does not need them).
+// ---------------------------------------------------------------------------
+// Generic N x N / d x d path (Cholesky based), in three parts so that the
+// receiver half and the weight half of one user can run on two threads:
+//   k1_part_u : A = T_k + σ² I = L_A L_A^H,  U = A^{-1} G_kk (solvers.py:210-225),
+//               T = I − U^H G_kk (solvers.py:242) and f_after_u (MSE matrix E = herm(T))
+//   k1_part_w : C = A − G_kk G_kk^H (interference + noise) = L_C L_C^H,
+//               W = I + Y^H Y with Y = L_C^{-1} G_kk
+//   k1_combine: W (weighted stage) or I, ln det W, the ill-conditioning test,
+//               f_after_w, P = α U W and D = −P T
+// W = T^{-1} at the MMSE receiver by the Woodbury identity
+//   (I − G^H A^{-1} G)^{-1} = I + G^H (A − G G^H)^{-1} G,
+// and ln det W = ln det A − ln det C (determinant lemma): the weight update of
+// solvers.py:228-254 (np.linalg.solve(T, I), hermitianize) without forming or
+// factoring T, and independent of the receiver half.  W is Hermitian by
+// construction and PD iff C is; the cond > 1e12 test uses ‖T‖_F ‖W‖_F.
+// ---------------------------------------------------------------------------
+// Re Tr(W E) with E = herm(T) (E[q][p] formed on the fly, same arithmetic as
+// storing E first)
+template <int DD>
+__device__ __forceinline__ double trace_w_herm(const cd (&W)[DD][DD], const cd (&T)[DD][DD]) {
+  double tr = 0.0;
+#pragma unroll
+  for (int p = 0; p < DD; ++p)
+#pragma unroll
+    for (int q = 0; q < DD; ++q) {
+      const double er = 0.5 * (T[q][p].r + T[p][q].r), ei = 0.5 * (T[q][p].i - T[p][q].i);
+      tr += W[p][q].r * er - W[p][q].i * ei;
+    }
+  return tr;
+}
+
 template <int NN, int DD>
-__device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[NN][DD],
-                                        double sigma2, double ak, const cd (&Wprev)[DD][DD],
-                                        double lndet_wprev, bool weighted, bool want_f,
-                                        K1Out<NN, DD>& o) {
-  if constexpr (NN == 2 && DD == 2) {
-    k1_math_22(Tg, Gkk, sigma2, ak, Wprev, lndet_wprev, weighted, want_f, o);
-    return;
-  }
-  cd A[NN][NN];
+struct K1U {
+  cd U[NN][DD];
+  cd T[DD][DD];    // E = herm(T) is formed on the fly where needed
+  double piv[NN];  // Cholesky pivots of A
+  double fu;
+  int status;
+};
+
+template <int NN, int DD>
+struct K1W {
+  cd W[DD][DD];
+  double piv[NN];  // Cholesky pivots of C
+  int pd;
+};
+
+template <int NN, int DD>
+__device__ __forceinline__ void k1_part_u(const cd (&Tg)[NN][NN], const cd (&Gkk)[NN][DD],
+                                          double sigma2, double ak, const cd (&Wprev)[DD][DD],
+                                          double lndet_wprev, bool want_f, K1U<NN, DD>& o) {
+  cd L[NN][NN];
 #pragma unroll
   for (int a = 0; a < NN; ++a)
 #pragma unroll
-    for (int b = 0; b < NN; ++b) A[a][b] = Tg[a][b];
+    for (int b = 0; b < NN; ++b) L[a][b] = Tg[a][b];
 #pragma unroll
-  for (int a = 0; a < NN; ++a) A[a][a].r += sigma2;
-  cd Lc[NN][NN];
+  for (int a = 0; a < NN; ++a) L[a][a].r += sigma2;
+  o.status = chol_lower<NN>(L) ? 0 : AMMMSE_STATUS_NONFINITE;
 #pragma unroll
-  for (int a = 0; a < NN; ++a)
-#pragma unroll
-    for (int b = 0; b < NN; ++b) Lc[a][b] = A[a][b];
-  o.status = 0;
-  if (!chol_lower<NN>(Lc)) o.status = AMMMSE_STATUS_NONFINITE;
+  for (int a = 0; a < NN; ++a) o.piv[a] = L[a][a].r;
 #pragma unroll
   for (int a = 0; a < NN; ++a)
 #pragma unroll
     for (int s = 0; s < DD; ++s) o.U[a][s] = Gkk[a][s];
-  chol_solve<NN, DD>(Lc, o.U);  // U = A^{-1} G_kk (cho_solve)
-  // T = I − U^H G_kk  (solvers.py:242)
-  cd T[DD][DD];
+  chol_solve<NN, DD>(L, o.U);  // U = A^{-1} G_kk (cho_solve)
 #pragma unroll
   for (int p = 0; p < DD; ++p)
 #pragma unroll
@@ -244,83 +278,110 @@ __device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[
       cd s = cmk(0.0);
 #pragma unroll
       for (int a = 0; a < NN; ++a) cfmac(s, o.U[a][p], Gkk[a][q]);
-      T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
+      o.T[p][q] = csub(cmk(p == q ? 1.0 : 0.0), s);
     }
   // MSE matrix E = I − U^H G_kk − G_kk^H U + U^H A U at the MMSE receiver:
   // U^H A U = U^H G_kk, so E = T^H (Hermitian part used, as in the 2x2 path)
-  cd E[DD][DD];
+  o.fu = 0.0;
   if (want_f) {
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q)
-        E[p][q] = cmk(0.5 * (T[p][q].r + T[q][p].r), 0.5 * (T[p][q].i - T[q][p].i));
-    double tr = 0.0;  // Tr(W_prev E): f_after_u uses the previous W (solvers.py:447)
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) tr += Wprev[p][q].r * E[q][p].r - Wprev[p][q].i * E[q][p].i;
+    const double tr = trace_w_herm<DD>(Wprev, o.T);  // f_after_u uses the previous W (solvers.py:447)
     o.fu = ak * (tr - lndet_wprev);
-  } else {
-    o.fu = 0.0;
   }
+}
+
+template <int NN, int DD>
+__device__ __forceinline__ void k1_part_w(const cd (&Tg)[NN][NN], const cd (&Gkk)[NN][DD],
+                                          double sigma2, K1W<NN, DD>& o) {
+  cd L[NN][NN];  // lower triangle of C = T_k + σ² I − G_kk G_kk^H
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      cd own = cmk(0.0);
+#pragma unroll
+      for (int s = 0; s < DD; ++s) own = cadd(own, cmulcb(Gkk[a][s], Gkk[b][s]));
+      L[a][b] = csub(Tg[a][b], own);
+    }
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    L[a][a].r += sigma2;
+    L[a][a].i = 0.0;
+  }
+  o.pd = chol_lower<NN>(L) ? 1 : 0;
+#pragma unroll
+  for (int a = 0; a < NN; ++a) o.piv[a] = L[a][a].r;
+  cd Y[NN][DD];  // Y = L_C^{-1} G_kk (forward substitution)
+#pragma unroll
+  for (int s = 0; s < DD; ++s)
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+      cd t = Gkk[i][s];
+#pragma unroll
+      for (int p = 0; p < i; ++p) t = csub(t, cmul(L[i][p], Y[p][s]));
+      Y[i][s] = cscale(t, 1.0 / L[i][i].r);
+    }
+#pragma unroll
+  for (int p = 0; p < DD; ++p)
+#pragma unroll
+    for (int q = p; q < DD; ++q) {  // W = I + Y^H Y, Hermitian by construction
+      cd s = cmk(p == q ? 1.0 : 0.0);
+#pragma unroll
+      for (int a = 0; a < NN; ++a) cfmac(s, Y[a][p], Y[a][q]);
+      if (p == q) s.i = 0.0;
+      o.W[p][q] = s;
+      o.W[q][p] = cconj(s);
+    }
+}
+
+template <int NN, int DD>
+__device__ __forceinline__ void k1_combine(const K1U<NN, DD>& u, const cd (&Wm)[DD][DD],
+                                           const double (&pivc)[NN], int pdc, double ak,
+                                           bool weighted, bool want_f, K1Out<NN, DD>& o) {
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int s = 0; s < DD; ++s) o.U[a][s] = u.U[a][s];
+  o.status = u.status;
+  o.fu = u.fu;
   o.lndetw = 0.0;
   if (weighted) {
-    // W = herm(T^{-1}) (np.linalg.solve(T, I) then hermitianize, linalg.py:12-14).
-    // T's anti-Hermitian part is rounding-level at the MMSE point, and
-    // herm(T^{-1}) = herm(T)^{-1} to second order in it, so W is formed from
-    // one Cholesky factorisation of herm(T): W = L^{-H} L^{-1}.  The same
-    // factor gives ln det W = -ln det herm(T) and the PD test of W
-    // (eigvalsh(W)[0] > 0, solvers.py:249-252): W is PD iff herm(T) is.
-    cd LT[DD][DD];
-    double nT = 0.0;
+    double nT = 0.0, nW = 0.0;
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q) {
-        nT += cabs2(T[p][q]);
-        LT[p][q] = cmk(0.5 * (T[p][q].r + T[q][p].r), 0.5 * (T[p][q].i - T[q][p].i));
+        nT += cabs2(u.T[p][q]);
+        nW += cabs2(Wm[p][q]);
+        o.W[p][q] = Wm[p][q];
       }
-    const bool pd = chol_lower<DD>(LT);
-    cd Ti[DD][DD];
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) Ti[p][q] = cmk(p == q ? 1.0 : 0.0);
-    double nTi = 0.0;
-    if (pd) {
-      chol_solve<DD, DD>(LT, Ti);
-#pragma unroll
-      for (int p = 0; p < DD; ++p)
-#pragma unroll
-        for (int q = 0; q < DD; ++q) nTi += cabs2(Ti[p][q]);
-    }
-    // ‖T‖_F ‖T^{-1}‖_F: an upper bound (within a factor d) of np.linalg.cond
-    const double cond = sqrt(nT) * sqrt(nTi);
-    if ((!pd || !isfinite(cond) || cond > kCondLimitUA) && o.status == 0)
+    // ‖T‖_F ‖W‖_F: an upper bound (within a factor d) of np.linalg.cond(T)
+    const double cond = sqrt(nT) * sqrt(nW);
+    if ((!pdc || !isfinite(cond) || cond > kCondLimitUA) && o.status == 0)
       o.status = AMMMSE_STATUS_ILL_CONDITIONED;
+    if (pdc && u.status == 0) {  // ln det W = ln det A − ln det C, one log
+      double q = 1.0;
 #pragma unroll
-    for (int p = 0; p < DD; ++p)
+      for (int j = 0; j < NN; ++j) {
+        const double r = u.piv[j] / pivc[j];
+        q *= r * r;
+      }
+      if (q >= 2.2250738585072014e-308 && q <= 1.7976931348623157e308) {
+        o.lndetw = log(q);
+      } else {
+        double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < DD; ++q)
-        o.W[p][q] = cmk(0.5 * (Ti[p][q].r + Ti[q][p].r), 0.5 * (Ti[p][q].i - Ti[q][p].i));
-    if (pd) o.lndetw = -chol_lndet<DD>(LT);
+        for (int j = 0; j < NN; ++j) s += log(u.piv[j]) - log(pivc[j]);
+        o.lndetw = 2.0 * s;
+      }
+    }
   } else {
 #pragma unroll
     for (int p = 0; p < DD; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q) o.W[p][q] = cmk(p == q ? 1.0 : 0.0);
   }
-  if (want_f) {
-    double tr = 0.0;
-#pragma unroll
-    for (int p = 0; p < DD; ++p)
-#pragma unroll
-      for (int q = 0; q < DD; ++q) tr += o.W[p][q].r * E[q][p].r - o.W[p][q].i * E[q][p].i;
-    o.fw = ak * (tr - o.lndetw);
-  } else {
-    o.fw = 0.0;
-  }
+  o.fw = 0.0;
+  if (want_f) o.fw = ak * (trace_w_herm<DD>(o.W, u.T) - o.lndetw);
 #pragma unroll
   for (int a = 0; a < NN; ++a)
 #pragma unroll
@@ -336,9 +397,34 @@ __device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[
     for (int q = 0; q < DD; ++q) {
       cd acc = cmk(0.0);
 #pragma unroll
-      for (int p = 0; p < DD; ++p) cfma(acc, o.P[a][p], T[p][q]);
+      for (int p = 0; p < DD; ++p) cfma(acc, o.P[a][p], u.T[p][q]);
       o.D[a][q] = cmk(-acc.r, -acc.i);
     }
+}
+
+// weighted: W update (else W = I).  want_f: compute f_after_u / f_after_w
+// terms (the exit residual pass does not need them).  One thread per user.
+template <int NN, int DD>
+__device__ __forceinline__ void k1_math(const cd (&Tg)[NN][NN], const cd (&Gkk)[NN][DD],
+                                        double sigma2, double ak, const cd (&Wprev)[DD][DD],
+                                        double lndet_wprev, bool weighted, bool want_f,
+                                        K1Out<NN, DD>& o) {
+  if constexpr (NN == 2 && DD == 2) {
+    k1_math_22(Tg, Gkk, sigma2, ak, Wprev, lndet_wprev, weighted, want_f, o);
+    return;
+  } else {
+    K1U<NN, DD> u;
+    k1_part_u<NN, DD>(Tg, Gkk, sigma2, ak, Wprev, lndet_wprev, want_f, u);
+    if (weighted) {
+      K1W<NN, DD> w;
+      k1_part_w<NN, DD>(Tg, Gkk, sigma2, w);
+      k1_combine<NN, DD>(u, w.W, w.piv, w.pd, ak, true, want_f, o);
+    } else {
+      const cd (&Wm)[DD][DD] = u.T;  // unused when not weighted
+      const double (&pv)[NN] = u.piv;
+      k1_combine<NN, DD>(u, Wm, pv, 1, ak, false, want_f, o);
+    }
+  }
 }
 
 // Rate (clipped at 0, in nats, times alpha) and f_after_v term of user k.

@@ -11,9 +11,14 @@ sweep point instead of one process-pool job per realization
                           output_dir="out")
     summary = run_experiment(spec)
 
+``verify=True`` runs the reference's oracles (harness.py:459-460, :509-517,
+:540-545) at batch scale on the device (verify.py): every realization is solved
+with recorded iterates, the four lemma-bound families are scanned over all of
+them in one pass per sweep point, and the finite-difference gradient check
+runs on the base system.
+
 Differences from the reference, by design:
   * only ``Algorithm.AMMMSE`` (the exact drivers are out of scope);
-  * ``verify=True`` (lemma-bound / finite-difference oracles) is rejected;
   * ``parallel_workers`` is kept for the schema but unused (one device call
     per point);
   * failure strings carry the reference's exception class and the engine's
@@ -192,6 +197,7 @@ class RunSummary:
 
     spec: ExperimentSpec
     points: tuple
+    oracle_reports: tuple = ()
 
     def to_json_dict(self, include_timing: bool = False) -> dict:
         points = []
@@ -215,7 +221,10 @@ class RunSummary:
                      "parallel_workers": self.spec.parallel_workers,
                      "output_dir": str(self.spec.output_dir)},
             "points": points,
-            "oracles": [],
+            "oracles": [{"name": r.name, "max_abs_error": r.max_abs_error,
+                         "max_rel_error": r.max_rel_error, "instances": r.instances,
+                         "passed": r.passed, "tolerance": r.tolerance, "detail": r.detail}
+                        for r in self.oracle_reports],
             "stamps": {"package": "paper_2510_20507_b200", "version": __version__,
                        "python": platform.python_version(), "numpy": np.__version__,
                        "rng": RNG_ALGORITHM},
@@ -249,20 +258,46 @@ def _failure(status: int, gamma, omega) -> str:
     return f"status {status}"
 
 
+def _lemma_point_report(label, H, s2, alpha, p_max, res, device):
+    """lemma_bounds[label]: check_lemma_bounds of every completed realization of
+    the point merged as harness._merge_lemma_reports does (harness.py:434-445),
+    in one batched device scan; bounds per realization from ammmse_bounds."""
+    import torch
+
+    from .solvers import engine
+    from .verify import lemma_bound_scan, lemma_report
+
+    ok = np.nonzero(res.status == STATUS_OK)[0]
+    if ok.size == 0:
+        return []
+    eng = engine(device)
+    dev = eng.device
+    Hd = torch.from_numpy(np.ascontiguousarray(H[ok])).to(dev)
+    s2d = torch.from_numpy(np.ascontiguousarray(s2[ok], dtype=np.float64)).to(dev)
+    ald = torch.from_numpy(np.ascontiguousarray(alpha[ok], dtype=np.float64)).to(dev)
+    pmd = torch.full((ok.size,), float(p_max), dtype=torch.float64, device=dev)
+    bnd = eng.bounds(Hd, ald, pmd, s2d)
+    U, W, V = (torch.from_numpy(np.ascontiguousarray(x[ok])).to(dev) for x in res.iterates)
+    worst, lim = lemma_bound_scan(Hd, s2d, ald, bnd, U, W, V, res.iterations[ok])
+    return [lemma_report(worst, lim, instances=int(res.iterations[ok].sum()),
+                         name=f"lemma_bounds[{label}]")]
+
+
 def run_experiment(spec: ExperimentSpec, verify: bool = False, dtype=np.complex128,
                    device=None) -> RunSummary:
     """Run every (sweep point x realization), write traces and summaries
     (harness.py:448-562), one batched device solve per sweep point.
     Realizations are reduced in realization order, so the outputs do not depend
     on the batch split."""
-    if verify:
-        raise ConfigError("verify oracles are not provided by the batched engine (SURVEY.md §8(f))")
     if spec.solver.algorithm is not Algorithm.AMMMSE:
         raise ConfigError("the batched engine runs A-MMMSE only")
     outdir = spec.output_dir
     outdir.mkdir(parents=True, exist_ok=True)
     options = spec.solver
+    if verify and not options.record_iterates:  # harness.py:459-460
+        options = dataclasses.replace(options, record_iterates=True)
     summaries = []
+    oracle_reports = []
     for label, point_cfg in sweep_points(spec):
         opts = options
         if options.gamma is None or options.omega is None:  # per point (harness.py:466-472)
@@ -275,6 +310,9 @@ def run_experiment(spec: ExperimentSpec, verify: bool = False, dtype=np.complex1
         res = run_ammmse_batch(H, s2, point_cfg.p_max, alpha, V0, opts, snr_db=point_cfg.snr_db,
                                record_trace=True, device=device)
         wall = (time.perf_counter() - t0) / spec.n_realizations
+        if verify:  # lemma bounds over every completed realization's iterates (:509-517)
+            oracle_reports.extend(_lemma_point_report(label, H, s2, alpha, point_cfg.p_max, res,
+                                                      device))
         wsr, iters, switches, residuals, walls, failures = [], [], [], [], [], []
         n_conv = 0
         for r in range(spec.n_realizations):
@@ -301,7 +339,13 @@ def run_experiment(spec: ExperimentSpec, verify: bool = False, dtype=np.complex1
             iterations_mean=im, iterations_std=isd, switch_iteration_mean=sm,
             stationarity_residual_max=max(residuals) if residuals else None,
             failures=tuple(failures), wall_time_mean=tm, wall_time_std=tsd))
-    summary = RunSummary(spec=spec, points=tuple(summaries))
+    if verify:  # finite-difference gradient check on the base system (:543-545)
+        from .verify import gradient_fd_report
+
+        fd = gradient_fd_report(spec.base)
+        if fd is not None:
+            oracle_reports.append(fd)
+    summary = RunSummary(spec=spec, points=tuple(summaries), oracle_reports=tuple(oracle_reports))
     (outdir / "summary.json").write_text(
         json.dumps(summary.to_json_dict(include_timing=False), indent=2, sort_keys=True) + "\n")
     timing = {"note": "wall-clock statistics are non-normative and excluded from the "

@@ -22,12 +22,14 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 from enum import Enum
+from typing import NamedTuple
 
 import numpy as np
 
 from . import _native
 from .errors import ConfigError, NativeLibraryError, raise_for_status
-from .model import ChannelSet, PrecoderSet, Stage, SystemConfig, init_precoders, project_sum_power
+from .model import (ChannelSet, PrecoderSet, ReceiverSet, Stage, SystemConfig, WeightMatrixSet,
+                    init_precoders, project_sum_power)
 
 GAMMA_SAFE = "safe"
 
@@ -62,7 +64,9 @@ class SolverOptions:
     """Options of one solve (ref solvers.py:88-136, same fields and checks).
 
     ``bisect_*`` belong to the exact drivers and are accepted but unused by
-    A-MMMSE; ``record_iterates`` is not supported by the device engine.
+    A-MMMSE; ``record_iterates`` keeps every (U, W, V_new) block iterate in
+    device buffers of (B, max_iters, ...) complex128 (meant for small B: the
+    bound scans of verify.py).
     """
 
     algorithm: Algorithm = Algorithm.WMMSE
@@ -120,6 +124,14 @@ class IterationRecord:
     f_after_w: float
     f_after_v: float
     rel_change: float
+
+
+class BlockIterate(NamedTuple):
+    """Full block variables of one completed iteration (ref solvers.py:159-164)."""
+
+    receivers: ReceiverSet
+    weight_matrices: WeightMatrixSet
+    precoders: PrecoderSet
 
 
 @dataclass(frozen=True, eq=False)
@@ -193,6 +205,8 @@ class BatchResult:
     gamma_used: object
     trace: object = None
     omega: float = 0.0
+    # recorded iterates (record_iterates): (U (B,T,K,N,d), W (B,T,K,d,d), V (B,T,K,M,d)) complex128
+    iterates: tuple | None = None
 
     def to_host(self) -> "BatchResult":
         def h(x):
@@ -202,7 +216,8 @@ class BatchResult:
 
         return BatchResult(*(h(getattr(self, f)) for f in (
             "final_precoders", "wsr_bits", "iterations", "converged", "stationarity_residual",
-            "switch_iteration", "status", "gamma_used", "trace")), omega=self.omega)
+            "switch_iteration", "status", "gamma_used", "trace")), omega=self.omega,
+            iterates=None if self.iterates is None else tuple(h(x) for x in self.iterates))
 
     def solve_result(self, i: int) -> SolveResult:
         """Per-realization SolveResult view (needs a host result with a trace)."""
@@ -217,6 +232,15 @@ class BatchResult:
                 f_after_u=float(row[5]), f_after_w=float(row[6]), f_after_v=float(row[7]),
                 rel_change=float(row[8])) for row in rows)
         sw = int(h.switch_iteration[i])
+        iterates = None
+        if h.iterates is not None:
+            U, W, V = h.iterates
+            stages = [records[t].stage if records else Stage.WEIGHTED for t in range(n)]
+            iterates = tuple(BlockIterate(
+                ReceiverSet(U[i, t]),
+                WeightMatrixSet(W[i, t], stages[t]) if stages[t] is Stage.WEIGHTED
+                else WeightMatrixSet.identity(W.shape[2], W.shape[3]),
+                PrecoderSet(V[i, t])) for t in range(n))
         return SolveResult(
             final_precoders=PrecoderSet(h.final_precoders[i]),
             trace=records,
@@ -224,6 +248,7 @@ class BatchResult:
             converged=bool(h.converged[i]),
             stationarity_residual=float(h.stationarity_residual[i]),
             switch_iteration=None if sw < 0 else sw,
+            iterates=iterates,
         )
 
 
@@ -307,6 +332,16 @@ class AmmmseEngine:
                     or not t.is_contiguous()):
                 raise ConfigError(f"out.{f} must be a contiguous {dt} tensor of shape {shape} on "
                                   f"{self.device}")
+        if out.iterates is not None:
+            K, M, d = init_precoders.shape[1], init_precoders.shape[2], init_precoders.shape[3]
+            U, W, V = out.iterates
+            N = U.shape[3] if U.dim() == 5 else -1
+            for nm, t, shape in (("U", U, (B, max_iters, K, N, d)), ("W", W, (B, max_iters, K, d, d)),
+                                 ("V", V, (B, max_iters, K, M, d))):
+                if (tuple(t.shape) != shape or t.dtype != torch.complex128 or t.device != self.device
+                        or not t.is_contiguous()):
+                    raise ConfigError(f"out.iterates {nm} must be a contiguous complex128 tensor of "
+                                      f"shape {shape}")
         if out.trace is not None:
             shape = (B, max_iters, _native.TRACE_FIELDS)
             if (tuple(out.trace.shape) != shape or out.trace.dtype != torch.float64
@@ -315,6 +350,7 @@ class AmmmseEngine:
 
     def solve(self, channels, noise_power, p_max, weights, init_precoders, *, gamma, omega,
               eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
+              record_iterates=False,
               out: BatchResult | None = None, stream=None, cluster_size: int = 0,
               h_placement: int = 0, tensor_cores: int = 0, workspace=None) -> BatchResult:
         torch = _torch()
@@ -348,6 +384,10 @@ class AmmmseEngine:
                 trace=(torch.full((B, int(max_iters), _native.TRACE_FIELDS), float("nan"),
                                   dtype=torch.float64, device=dev) if record_trace else None),
             )
+            if record_iterates:
+                T, N, d, M = int(max_iters), dims.N, dims.d, dims.M
+                z = lambda *s: torch.full(s, complex("nan+nanj"), dtype=torch.complex128, device=dev)
+                out.iterates = (z(B, T, K, N, d), z(B, T, K, d, d), z(B, T, K, M, d))
         # gamma: float | "safe" | (B,) float64 tensor;  omega: float | (B,) float64 tensor
         g_arr = gamma if torch.is_tensor(gamma) else None
         o_arr = omega if torch.is_tensor(omega) else None
@@ -369,10 +409,11 @@ class AmmmseEngine:
                                      None if g_arr is None else g_arr.data_ptr(),
                                      None if o_arr is None else o_arr.data_ptr())
         ptr = lambda t: None if t is None else t.data_ptr()
+        its = out.iterates if out.iterates is not None else (None, None, None)
         res = _native.AmmmseResult(
             ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
             ptr(out.stationarity_residual), ptr(out.switch_iteration), ptr(out.status),
-            ptr(out.gamma_used), ptr(out.trace))
+            ptr(out.gamma_used), ptr(out.trace), ptr(its[0]), ptr(its[1]), ptr(its[2]))
         with torch.cuda.device(dev):  # the C-ABI launches on the current device
             ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
             if ws_bytes == 0:
@@ -584,8 +625,6 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
     torch = _torch()
     if options.algorithm is not Algorithm.AMMMSE:
         raise ConfigError("options.algorithm must be AMMMSE")
-    if options.record_iterates:
-        raise ConfigError("record_iterates is not supported by the batched device engine")
     H = np.asarray(channels)
     V0 = np.asarray(init_precoders)
     if H.ndim != 4 or V0.ndim != 4:
@@ -615,7 +654,8 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
                     torch.from_numpy(pm).to(dev), torch.from_numpy(al).to(dev),
                     torch.from_numpy(V0).to(dev), gamma=gamma, omega=omega, eps1=options.eps1,
                     eps2=options.eps2, max_iters=options.max_iters, latch_stage=options.latch_stage,
-                    record_trace=record_trace, cluster_size=cluster_size,
+                    record_trace=record_trace or options.record_iterates,
+                    record_iterates=options.record_iterates, cluster_size=cluster_size,
                     h_placement=h_placement, tensor_cores=tensor_cores)
     return out.to_host()
 

@@ -216,10 +216,13 @@ def test_cluster_streamed_odd_stage_rows_complex64(cuda):
         assert rel.max() <= WSR_RTOL_C64, (hp, rel)
 
 
-@pytest.mark.parametrize("M,K,N,d,csize", [(128, 16, 4, 4, 2), (256, 32, 2, 2, 2), (128, 32, 2, 2, 1)])
+@pytest.mark.parametrize("M,K,N,d,csize", [(128, 16, 4, 4, 2), (256, 32, 2, 2, 4), (128, 32, 2, 2, 1),
+                                           (128, 32, 4, 4, 4), (64, 16, 4, 4, 2)])
 def test_cluster_tensor_core_gemms_complex64(cuda, M, K, N, d, csize):
-    """tcgen05 3xTF32 GEMMs (tensor_cores=1) against the fp64 oracle and the FFMA
-    path on the same inputs (M >= 128 shapes the tensor-core mode accepts)."""
+    """tcgen05 3xTF32 GEMMs (tensor_cores=1: bulk-copied pre-split H planes, TMEM
+    accumulators) against the fp64 oracle and the FFMA path on the same inputs,
+    including the BASELINE large shape (M=128, K=32, N=d=4 on 4-CTA clusters)
+    and a 64-row UMMA tile (KN = 64)."""
     b = build_batch(M, N, K, d, 3, p_max=50.0, weights="uniform", dtype=np.complex64, seed0=21)
     kw = dict(gamma=0.002, omega=0.8, eps2=1e-5, max_iters=120)
     opts = SolverOptions(algorithm="ammmse", **kw)

@@ -68,10 +68,8 @@ class TestSpec:
         with pytest.raises(ConfigError):
             dataclasses.replace(s, **kw)
 
-    def test_verify_and_other_algorithms_rejected(self, tmp_path):
+    def test_other_algorithms_rejected(self, tmp_path):
         s = _spec(tmp_path)
-        with pytest.raises(ConfigError):
-            H.run_experiment(s, verify=True)
         with pytest.raises(ConfigError):
             H.run_experiment(dataclasses.replace(s, solver=dataclasses.replace(s.solver,
                                                                                algorithm="wmmse")))
