@@ -6,7 +6,7 @@ PHASES ?= 0
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v -DAMMMSE_PHASES=$(PHASES)
 SRC_DIR := paper_2510_20507_b200/csrc
 OBJ_DIR := build/obj
-SRCS := $(SRC_DIR)/ammmse_capi.cu $(SRC_DIR)/ammmse_gen.cu $(wildcard $(SRC_DIR)/inst/*.cu)
+SRCS := $(SRC_DIR)/ammmse_capi.cu $(SRC_DIR)/ammmse_gen.cu $(SRC_DIR)/exact_engine.cu $(wildcard $(SRC_DIR)/inst/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS := include/ammmse.h $(wildcard $(SRC_DIR)/*.cuh) $(SRC_DIR)/entries.h
 LIB := paper_2510_20507_b200/libammmse.so

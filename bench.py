@@ -475,18 +475,39 @@ def main():
     peak = peak32 if w.dtype == np.complex64 else peak64
     sm_mhz = (clk.get("sm_max_mhz") or 1965.0)
     nominal = 148 * 128 * 2 * sm_mhz * 1e6 if w.dtype == np.complex64 else 148 * 64 * 2 * sm_mhz * 1e6
-    roofline = {
-        "bound": "fma", "pipe": "fp32 FFMA (CUDA cores)" if w.dtype == np.complex64 else "fp64 DFMA",
-        "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-        "frac": achieved / peak if peak > 0 else None, "traffic": None,
-        "peak_source": "measured live by libammmse_probe (register FFMA/DFMA throughput kernel); "
-                       "MEASURED_PEAKS.json has no FP32 entry",
-        "peak_nominal": nominal / 1e12, "frac_of_nominal": achieved / nominal,
+    kname = ("ammmse_cluster_kernel" if engine_plan["cluster"] else "ammmse_solve_kernel")
+    kname += (f"<C={engine_plan['cluster']}>" if engine_plan["cluster"] else "")
+    if engine_plan["tensor_cores"]:
+        # tcgen05 3xTF32 GEMMs: the bound is the tensor pipe; its fp32-equivalent
+        # peak = dense tf32 (measured bf16 burst / 2) / 3 products per real product
+        mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        bf16 = json.load(open(mp))["bf16_tflops"] if os.path.exists(mp) else 1590.0
+        tpeak = bf16 / 2 / 3 * 1e12
+        roofline = {
+            "bound": "tensor", "pipe": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate)",
+            "achieved": achieved / 1e12, "peak": tpeak / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / tpeak, "traffic": None,
+            "peak_source": f"MEASURED_PEAKS.json bf16 burst {bf16} TF / 2 (dense tf32) / 3 (3xTF32)"
+                           + ("" if os.path.exists(mp) else " [fallback 1590]"),
+            "ffma_peak_probe": peak / 1e12, "frac_of_ffma_probe": achieved / peak,
+            "ffma_peak_nominal": nominal / 1e12,
+        }
+    else:
+        roofline = {
+            "bound": "fma", "pipe": "fp32 FFMA (CUDA cores)" if w.dtype == np.complex64 else "fp64 DFMA",
+            "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak > 0 else None, "traffic": None,
+            "peak_source": "measured live by libammmse_probe (register FFMA/DFMA throughput kernel); "
+                           "MEASURED_PEAKS.json has no FP32 entry",
+            "peak_nominal": nominal / 1e12, "frac_of_nominal": achieved / nominal,
+        }
+    roofline.update({
         "per": "GPU (achieved = whole-job flops / max-over-ranks time / N)",
         "work": f"F=16*K^2*N*d*M={fpu:.0f} flop per realization-iteration x {iters_total} "
-                f"realization-iterations per launch",
-        "kernel": "ammmse_solve_kernel (1 launch per step)",
-    }
+                f"realization-iterations per launch (whole solve counted at GEMM flops)",
+        "kernel": f"{kname} (1 launch per step)",
+        "gemm_step": "bench_gemmstep.py / profiles/r02_gemmstep.md: the GEMM step alone",
+    })
 
     # BCGD-step share of the kernel (GEMM-step fraction =
     # F x realization-iterations / t_GEMM / peak): one extra, untimed solve with

@@ -116,9 +116,10 @@ typedef struct AmmmseOptions {
   int32_t h_placement; /* cluster engine only: 0 auto, 1 H resident in every CTA's SMEM,
                           2 H streamed from HBM/L2 through a cp.async ring, 3 streamed H and
                           the previous precoders in a per-CTA global scratch slot */
-  int32_t tensor_cores;/* cluster engine, complex64: 1 tcgen05 3xTF32 GEMMs (streamed H planes,
-                          TMEM accumulators) where shape and shared memory allow; 0 / 2 FP32
-                          FFMA GEMMs (0 = automatic = FFMA: measured faster in round 1) */
+  int32_t tensor_cores;/* cluster engine, complex64: 1 tcgen05 3xTF32 GEMMs (bulk-copied
+                          pre-split H planes, TMEM accumulators) where shape and shared memory
+                          allow; 2 FP32 FFMA GEMMs; 0 automatic (tensor cores for N = d = 4,
+                          where measured faster, else FFMA) */
 } AmmmseOptions;
 
 /* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */
@@ -187,6 +188,24 @@ const char* ammmse_error_string(int code);
 int ammmse_generate_iid(const AmmmseDims* dims, unsigned long long seed0, double p_max,
                         int uniform_weights, void* channels, void* init_precoders,
                         double* weights, void* stream);
+
+/* Exact-update drivers: replace run_wmmse / run_mmmse
+   (solvers.py:521-537 -> _run_bcd :415-518 with exact=True, no extrapolation):
+   MMSE receivers, the standard weight update (WMMSE: weighted from t = 1;
+   MMMSE: identity weights until the eps1 switch), and the exact precoder
+   update (A + lambda I)^{-1} B by dual bisection (bisect_dual :276-329,
+   update_precoders_exact :332-348).  fp64 throughout (complex64 inputs are
+   promoted).  Same problem / result layout as ammmse_solve; options.gamma,
+   gamma_safe, omega, cluster_size, h_placement, tensor_cores are ignored;
+   per-realization status as for ammmse_solve (no divergence test). */
+enum { AMMMSE_ALGO_WMMSE = 1, AMMMSE_ALGO_MMMSE = 2 };
+
+size_t ammmse_exact_workspace_size(const AmmmseDims* dims);
+
+int ammmse_solve_exact(const AmmmseDims* dims, const AmmmseProblem* problem,
+                       const AmmmseOptions* options, int algorithm, double bisect_tol,
+                       int bisect_max, AmmmseResult* result, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /* Diagnostics: the engine configuration ammmse_solve would launch for these
    dims / options.  info[8] = {cluster size (0 = single-CTA engine), H resident,

@@ -39,6 +39,9 @@ from .solvers import (
     resolve_step_parameters,
     run_ammmse,
     run_ammmse_batch,
+    run_exact_batch,
+    run_mmmse,
+    run_wmmse,
     solve,
 )
 

@@ -17,6 +17,8 @@ from .errors import NativeLibraryError
 LIB_PATH = pathlib.Path(__file__).resolve().with_name("libammmse.so")
 
 ABI_VERSION = 2
+ALGO_WMMSE = 1
+ALGO_MMMSE = 2
 COMPLEX64 = 0
 COMPLEX128 = 1
 TRACE_FIELDS = 9
@@ -39,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "ammmse_error_string",
     "ammmse_phase_profile",
     "ammmse_plan_info",
+    "ammmse_exact_workspace_size",
+    "ammmse_solve_exact",
     "ammmse_generate_iid",
 )
 
@@ -113,6 +117,13 @@ def lib() -> ctypes.CDLL:
         h.ammmse_solve.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.POINTER(AmmmseProblem),
                                    ctypes.POINTER(AmmmseOptions), ctypes.POINTER(AmmmseResult),
                                    ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        h.ammmse_exact_workspace_size.restype = ctypes.c_size_t
+        h.ammmse_exact_workspace_size.argtypes = [ctypes.POINTER(AmmmseDims)]
+        h.ammmse_solve_exact.restype = ctypes.c_int
+        h.ammmse_solve_exact.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.POINTER(AmmmseProblem),
+                                         ctypes.POINTER(AmmmseOptions), ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_int, ctypes.POINTER(AmmmseResult), ctypes.c_void_p,
+                                         ctypes.c_size_t, ctypes.c_void_p]
         h.ammmse_bounds.restype = ctypes.c_int
         h.ammmse_bounds.argtypes = [ctypes.POINTER(AmmmseDims), ctypes.c_void_p, ctypes.c_void_p,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,

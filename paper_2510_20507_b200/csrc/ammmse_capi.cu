@@ -112,12 +112,16 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_core
         continue;
       // streamed H moves 16-byte pieces: complex64 rows need an even length
       if (!hres && d->dtype == AMMMSE_COMPLEX64 && (d->M % 2)) continue;
-      // tensor-core GEMMs (streamed pre-split H planes): opt-in (tensor_cores = 1).
-      // Measured round 1: the one-K-step-per-stage ring is latency bound and
-      // slower than the FFMA path (large 407 vs 582 realizations/s), so the
-      // automatic plan keeps FFMA.
+      // tensor-core GEMMs (bulk-copied pre-split H planes, TMEM accumulators):
+      // forced with tensor_cores = 1; chosen automatically (tensor_cores = 0)
+      // where measured faster than the FFMA GEMMs: N = d = 4 (BASELINE large,
+      // 1185 vs 1052 realizations/s).  The N = d = 2 shapes keep FFMA (massive
+      // 733 vs 1045, sweep256 5.6k vs 8.1k: their FFMA GEMMs already run at
+      // 0.4 of the FMA peak while the per-chunk handoffs of the tensor-core
+      // ring are latency bound, bench_gemmstep.py).
       const int ncol = (d->K / c) * d->d;
-      if (!hres && d->dtype == AMMMSE_COMPLEX64 && tensor_cores == 1 &&
+      const bool tc_auto = tensor_cores == 0 && d->N == 4 && d->d == 4;
+      if (!hres && d->dtype == AMMMSE_COMPLEX64 && (tensor_cores == 1 || tc_auto) &&
           ammmse::tc_shape_ok(d->M, d->K * d->N, ncol)) {
         const size_t st = e->cluster_smem_bytes(d->M, d->K, c, hres, vglob, sb, 1);
         if (st <= (size_t)lim) {

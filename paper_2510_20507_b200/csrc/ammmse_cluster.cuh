@@ -769,10 +769,8 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
   // the SMEM slot 0 (vc = vx = 0, vo = 1, save): GEMM-B always reads SMEM.
   auto grad_step = [&](int ysrc, int vc, int vo, int vx, bool save, double step, double omega,
                        bool extrap) {
-    const R* vcr = Vr[vc];  // always shared memory (V_old is the only global slot)
+    const R* vcr = Vr[vc];
     const R* vci = Vi[vc];
-    AMMMSE_SHARED(vcr);
-    AMMMSE_SHARED(vci);
     R* vor = Vr[vo];
     R* voi = Vi[vo];
     R* xr = Vr[vx];
@@ -822,7 +820,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
       tcs::gemm(pipe, tc_seq, hpA, tmA, M / tmA, KN, ncol, (const float*)Gr[ysrc],
                 (const float*)Gi[ysrc], ldg);
       pre();
-      tcs::for_each(pipe, tmA, M / tmA, ncol, true,
+      tcs::for_each(pipe, tmA, M / tmA, ncol, KN, true,
                     [&](int p, int q, float gr, float gi) { epi(p, q, (R)gr, (R)gi); });
     } else if (hres)
       cgemm_any<R, 4, 4, true>(M, ncol, KN, Hr, Hi, ldh, Gr[ysrc], Gi[ysrc], ldg, epi);
@@ -853,15 +851,11 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     R* hr = ghat >= 0 ? Gr[ghat] : nullptr;
     R* hi = ghat >= 0 ? Gi[ghat] : nullptr;
     const R om = (R)omega;
-    AMMMSE_SHARED(gr);
-    AMMMSE_SHARED(gi);
     auto epi = [&](int p, int q, R cr, R ci) {
       const int o = p * ldg + q;
       gr[o] = cr;
       gi[o] = ci;
       if (hr) {  // ω = 0: plain copy (G_prev may be uninitialised shared memory)
-        AMMMSE_SHARED(hr);
-        AMMMSE_SHARED(hi);
         hr[o] = om == R(0) ? cr : cr + om * (cr - hr[o]);
         hi[o] = om == R(0) ? ci : ci + om * (ci - hi[o]);
       }
@@ -869,7 +863,7 @@ __global__ void __launch_bounds__(kClusterThreads<NN, DD>, 1) ammmse_cluster_ker
     if constexpr (TC) {  // G = H V on tcgen05, epilogue one thread per row
       tcs::gemm(pipe, tc_seq, hpB, tmB, KN / tmB, M, ncol, (const float*)Vr[src],
                 (const float*)Vi[src], ldv);
-      tcs::for_each(pipe, tmB, KN / tmB, ncol, false,
+      tcs::for_each(pipe, tmB, KN / tmB, ncol, M, false,
                     [&](int p, int q, float cr, float ci) { epi(p, q, (R)cr, (R)ci); });
     } else if (hres)
       cgemm_any<R, 2, 4, false>(KN, ncol, M, Hr, Hi, ldh, Vr[src], Vi[src], ldv, epi);

@@ -42,6 +42,12 @@ __host__ __device__ __forceinline__ uint32_t kstep_offset(int row, int kk) {
   return (uint32_t)(((row >> 3) * 2 + (kk >> 2)) * 128 + (row & 7) * 16 + (kk & 3) * 4);
 }
 
+// Accumulator sets of a gemm() call: 2 when both fit the 512 TMEM columns
+// (8 ncol columns per 128-row tile and set), else 1.
+__host__ __device__ __forceinline__ int accum_sets(int ncol, int nmt, int nch) {
+  return (2 * 8 * ncol * nmt <= 512 && nch >= 2) ? 2 : 1;
+}
+
 struct Pipe {
   unsigned char* ring;  // S stages of stage_bytes, 128-byte aligned
   int S;
@@ -124,6 +130,7 @@ __device__ __forceinline__ void gemm(const Pipe& p, Seq& sq, const float* __rest
   const uint32_t a_plane = (uint32_t)(rows * KW * 4);
   const int n4 = 4 * ncol;
   const uint32_t S = (uint32_t)p.S;
+  const int nsets = accum_sets(ncol, nmt, nch);
 
   if (warp >= pw0) {  // ---- producers: warp w fills chunks c = w - pw0 (mod #producer warps) ----
     const int nw = (int)(blockDim.x >> 5) - pw0;
@@ -175,10 +182,14 @@ __device__ __forceinline__ void gemm(const Pipe& p, Seq& sq, const float* __rest
       umma::fence_after();
       const uint32_t a0 = umma::smem_u32(stage_a(p, s));
       const uint64_t bd = umma::make_sdesc(umma::smem_u32(stage_b(p, s)), 128, 256);
-      const uint32_t acc = c > 0 ? 1u : 0u;
+      // chunk c accumulates into set c % nsets (split accumulation: the tensor
+      // core's fp32 accumulation error grows with the chain; the sets are
+      // summed in fp32 by the epilogue)
+      const int set = c % nsets;
+      const uint32_t acc = c >= nsets ? 1u : 0u;
       for (int t = 0; t < ((DBG & 4) ? 0 : nmt); ++t) {
         const uint32_t at = a0 + (uint32_t)t * (uint32_t)(tm / 8) * 256u;
-        const uint32_t d1 = p.tmem + (uint32_t)(8 * ncol * t);
+        const uint32_t d1 = p.tmem + (uint32_t)(8 * ncol * (t + nmt * set));
         const uint32_t d2 = d1 + (uint32_t)n4;
         umma::mma_tf32(d1, umma::make_sdesc(at, 128, 256), bd, id_all, acc);              // re_hi
         umma::mma_tf32(d1, umma::make_sdesc(at + 2 * a_plane, 128, 256), bd, id_hi, 1u);  // re_lo
@@ -212,6 +223,7 @@ __device__ __forceinline__ void gemm_sync(const Pipe& p, Seq& sq, const float* _
   const uint32_t a_plane = (uint32_t)(rows * KW * 4);
   const int n4 = 4 * ncol;
   const uint32_t S = (uint32_t)p.S;
+  const int nsets = accum_sets(ncol, nmt, nch);
   const uint32_t id_all = umma::make_idesc_tf32(tm, n4, false, false, false, false);
   const uint32_t id_hi = umma::make_idesc_tf32(tm, 2 * ncol, false, false, false, false);
   auto produce = [&](int c) {
@@ -249,10 +261,14 @@ __device__ __forceinline__ void gemm_sync(const Pipe& p, Seq& sq, const float* _
       umma::fence_after();
       const uint32_t a0 = umma::smem_u32(stage_a(p, s));
       const uint64_t bd = umma::make_sdesc(umma::smem_u32(stage_b(p, s)), 128, 256);
-      const uint32_t acc = c > 0 ? 1u : 0u;
+      // chunk c accumulates into set c % nsets (split accumulation: the tensor
+      // core's fp32 accumulation error grows with the chain; the sets are
+      // summed in fp32 by the epilogue)
+      const int set = c % nsets;
+      const uint32_t acc = c >= nsets ? 1u : 0u;
       for (int t = 0; t < nmt; ++t) {
         const uint32_t at = a0 + (uint32_t)t * (uint32_t)(tm / 8) * 256u;
-        const uint32_t d1 = p.tmem + (uint32_t)(8 * ncol * t);
+        const uint32_t d1 = p.tmem + (uint32_t)(8 * ncol * (t + nmt * set));
         const uint32_t d2 = d1 + (uint32_t)n4;
         umma::mma_tf32(d1, umma::make_sdesc(at, 128, 256), bd, id_all, acc);
         umma::mma_tf32(d1, umma::make_sdesc(at + 2 * a_plane, 128, 256), bd, id_hi, 1u);
@@ -277,7 +293,9 @@ __device__ __forceinline__ void gemm_sync(const Pipe& p, Seq& sq, const float* _
 // Warp w reads TMEM lane quadrant (w & 3); warps w >> 2 split the columns in
 // blocks of 16.  Ends with tcgen05.fence::before_thread_sync.
 template <class F>
-__device__ __forceinline__ void for_each(const Pipe& p, int tm, int nmt, int ncol, bool conj_a, F f) {
+__device__ __forceinline__ void for_each(const Pipe& p, int tm, int nmt, int ncol, int KD, bool conj_a,
+                                         F f) {
+  const int nsets = accum_sets(ncol, nmt, KD / KW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quad = warp & 3, cgrp = warp >> 2, ngrp = (int)(blockDim.x >> 7);
   for (int t = 0; t < nmt; ++t) {
@@ -287,29 +305,39 @@ __device__ __forceinline__ void for_each(const Pipe& p, int tm, int nmt, int nco
     else
       row = lane < 16 ? 16 * quad + lane : -1;  // M = 64: lanes 0-15 of each quadrant
     const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
-    const uint32_t d1 = p.tmem + lane_base + (uint32_t)(8 * ncol * t);
-    const uint32_t d2 = d1 + (uint32_t)(4 * ncol);
     for (int q0 = 16 * cgrp; q0 < ncol; q0 += 16 * ngrp) {
-      uint32_t rr_h[16], ri_h[16], rr_l[16], ri_l[16], ir_h[16], ii_h[16], ir_l[16], ii_l[16];
-      umma::tmem_ld16_nw(d1 + q0, rr_h);
-      umma::tmem_ld16_nw(d1 + ncol + q0, ri_h);
-      umma::tmem_ld16_nw(d1 + 2 * ncol + q0, rr_l);
-      umma::tmem_ld16_nw(d1 + 3 * ncol + q0, ri_l);
-      umma::tmem_ld16_nw(d2 + q0, ir_h);
-      umma::tmem_ld16_nw(d2 + ncol + q0, ii_h);
-      umma::tmem_ld16_nw(d2 + 2 * ncol + q0, ir_l);
-      umma::tmem_ld16_nw(d2 + 3 * ncol + q0, ii_l);
-      umma::tmem_wait_ld();
-      if (row >= 0) {
+      float prr[16], pri[16], pir[16], pii[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) prr[j] = pri[j] = pir[j] = pii[j] = 0.f;
+      for (int set = 0; set < nsets; ++set) {
+        const uint32_t d1 = p.tmem + lane_base + (uint32_t)(8 * ncol * (t + nmt * set));
+        const uint32_t d2 = d1 + (uint32_t)(4 * ncol);
+        uint32_t rr_h[16], ri_h[16], rr_l[16], ri_l[16], ir_h[16], ii_h[16], ir_l[16], ii_l[16];
+        umma::tmem_ld16_nw(d1 + q0, rr_h);
+        umma::tmem_ld16_nw(d1 + ncol + q0, ri_h);
+        umma::tmem_ld16_nw(d1 + 2 * ncol + q0, rr_l);
+        umma::tmem_ld16_nw(d1 + 3 * ncol + q0, ri_l);
+        umma::tmem_ld16_nw(d2 + q0, ir_h);
+        umma::tmem_ld16_nw(d2 + ncol + q0, ii_h);
+        umma::tmem_ld16_nw(d2 + 2 * ncol + q0, ir_l);
+        umma::tmem_ld16_nw(d2 + 3 * ncol + q0, ii_l);
+        umma::tmem_wait_ld();
         auto asf = [](uint32_t u) { return __uint_as_float(u); };
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float prr = asf(rr_h[j]) + asf(rr_l[j]), pri = asf(ri_h[j]) + asf(ri_l[j]);
-          const float pir = asf(ir_h[j]) + asf(ir_l[j]), pii = asf(ii_h[j]) + asf(ii_l[j]);
+          prr[j] += asf(rr_h[j]) + asf(rr_l[j]);
+          pri[j] += asf(ri_h[j]) + asf(ri_l[j]);
+          pir[j] += asf(ir_h[j]) + asf(ir_l[j]);
+          pii[j] += asf(ii_h[j]) + asf(ii_l[j]);
+        }
+      }
+      if (row >= 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
           if (conj_a)
-            f(row, q0 + j, prr + pii, pri - pir);
+            f(row, q0 + j, prr[j] + pii[j], pri[j] - pir[j]);
           else
-            f(row, q0 + j, prr - pii, pri + pir);
+            f(row, q0 + j, prr[j] - pii[j], pri[j] + pir[j]);
         }
       }
     }

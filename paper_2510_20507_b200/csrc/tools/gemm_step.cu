@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256, 1)
         tcs::gemm<7>(p, seq, hp, tm, rows / tm, kd, ncol, Bs, Bsi, ldb);
       else
         tcs::gemm(p, seq, hp, tm, rows / tm, kd, ncol, Bs, Bsi, ldb);
-      tcs::for_each(p, tm, rows / tm, ncol, mode == 1, [&](int row, int q, float re, float im) {
+      tcs::for_each(p, tm, rows / tm, ncol, kd, mode == 1, [&](int row, int q, float re, float im) {
         if (r == reps - 1) Dg[(size_t)row * ncol + q] = make_float2(re, im);
       });
       __syncthreads();

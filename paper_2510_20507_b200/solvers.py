@@ -352,7 +352,12 @@ class AmmmseEngine:
               eps1=0.1, eps2=1e-3, max_iters=1000, latch_stage=True, record_trace=False,
               record_iterates=False,
               out: BatchResult | None = None, stream=None, cluster_size: int = 0,
-              h_placement: int = 0, tensor_cores: int = 0, workspace=None) -> BatchResult:
+              h_placement: int = 0, tensor_cores: int = 0, workspace=None,
+              algorithm: str = "ammmse", bisect_tol: float = 1e-4,
+              bisect_max: int = 100) -> BatchResult:
+        """algorithm "ammmse" (ammmse_solve) or the exact-update drivers
+        "wmmse" / "mmmse" (ammmse_solve_exact: bisect_tol / bisect_max apply,
+        gamma / omega and the engine knobs are ignored)."""
         torch = _torch()
         dims = self.dims(channels, init_precoders)
         self.check(dims)
@@ -414,8 +419,13 @@ class AmmmseEngine:
             ptr(out.final_precoders), ptr(out.wsr_bits), ptr(out.iterations), ptr(out.converged),
             ptr(out.stationarity_residual), ptr(out.switch_iteration), ptr(out.status),
             ptr(out.gamma_used), ptr(out.trace), ptr(its[0]), ptr(its[1]), ptr(its[2]))
+        exact = {"ammmse": 0, "wmmse": _native.ALGO_WMMSE, "mmmse": _native.ALGO_MMMSE}.get(
+            str(algorithm).lower())
+        if exact is None:
+            raise ConfigError(f"unknown algorithm {algorithm!r}")
         with torch.cuda.device(dev):  # the C-ABI launches on the current device
-            ws_bytes = int(self.lib.ammmse_workspace_size_opts(dims, opts))
+            ws_bytes = int(self.lib.ammmse_exact_workspace_size(dims) if exact
+                           else self.lib.ammmse_workspace_size_opts(dims, opts))
             if ws_bytes == 0:
                 raise ConfigError(f"no engine configuration fits (cluster_size={cluster_size}, "
                                   f"h_placement={h_placement}, tensor_cores={tensor_cores})")
@@ -428,8 +438,13 @@ class AmmmseEngine:
                 ws = self._workspace(ws_bytes, stream)
             if stream is None:
                 stream = torch.cuda.current_stream(dev)
-            rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
-                                       ctypes_stream(stream))
+            if exact:
+                rc = self.lib.ammmse_solve_exact(dims, prob, opts, exact, float(bisect_tol),
+                                                 int(bisect_max), res, ws.data_ptr(), ws.numel(),
+                                                 ctypes_stream(stream))
+            else:
+                rc = self.lib.ammmse_solve(dims, prob, opts, res, ws.data_ptr(), ws.numel(),
+                                           ctypes_stream(stream))
         if rc != 0:
             if rc == _native.ERR_INVALID:
                 raise ConfigError(_native.error_string(rc))
@@ -625,6 +640,28 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
     torch = _torch()
     if options.algorithm is not Algorithm.AMMMSE:
         raise ConfigError("options.algorithm must be AMMMSE")
+    return _run_batch(channels, noise_power, p_max, weights, init_precoders, options, snr_db,
+                      record_trace, device, step_gamma, step_omega, cluster_size, h_placement,
+                      tensor_cores)
+
+
+def run_exact_batch(channels, noise_power, p_max, weights, init_precoders, options: SolverOptions,
+                    record_trace: bool = False, device=None) -> BatchResult:
+    """B realizations of the exact-update drivers run_wmmse / run_mmmse (ref
+    solvers.py:521-537) on the device (ammmse_solve_exact): host arrays in,
+    host BatchResult out, per-realization status codes; the algorithm,
+    eps1 / eps2 / max_iters / latch_stage / bisect_tol / bisect_max come from
+    ``options``."""
+    if options.algorithm not in (Algorithm.WMMSE, Algorithm.MMMSE):
+        raise ConfigError("options.algorithm must be WMMSE or MMMSE")
+    return _run_batch(channels, noise_power, p_max, weights, init_precoders, options, 10.0,
+                      record_trace, device, None, None, 0, 0, 0)
+
+
+def _run_batch(channels, noise_power, p_max, weights, init_precoders, options, snr_db,
+               record_trace, device, step_gamma, step_omega, cluster_size, h_placement,
+               tensor_cores) -> BatchResult:
+    torch = _torch()
     H = np.asarray(channels)
     V0 = np.asarray(init_precoders)
     if H.ndim != 4 or V0.ndim != 4:
@@ -637,7 +674,8 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
     pm = np.broadcast_to(np.asarray(p_max, dtype=np.float64), (B,)).copy()
     al = np.broadcast_to(np.asarray(weights, dtype=np.float64), (B, K)).copy()
     _validate_host_inputs(H, s2, pm, al, V0)
-    gamma, omega = resolve_step_parameters(options, snr_db)
+    exact = options.algorithm is not Algorithm.AMMMSE
+    gamma, omega = (0.0, 0.0) if exact else resolve_step_parameters(options, snr_db)
     eng = engine(device)
     dev = eng.device
     if step_gamma is not None:
@@ -656,7 +694,9 @@ def run_ammmse_batch(channels, noise_power, p_max, weights, init_precoders, opti
                     eps2=options.eps2, max_iters=options.max_iters, latch_stage=options.latch_stage,
                     record_trace=record_trace or options.record_iterates,
                     record_iterates=options.record_iterates, cluster_size=cluster_size,
-                    h_placement=h_placement, tensor_cores=tensor_cores)
+                    h_placement=h_placement, tensor_cores=tensor_cores,
+                    algorithm=options.algorithm.value, bisect_tol=options.bisect_tol,
+                    bisect_max=options.bisect_max)
     return out.to_host()
 
 
@@ -686,10 +726,51 @@ def run_ammmse(channels: ChannelSet, config: SystemConfig, options: SolverOption
     return res.solve_result(0)
 
 
+def _run_exact(channels: ChannelSet, config: SystemConfig, options: SolverOptions,
+               init=None) -> SolveResult:
+    if channels.noise_power is None:
+        raise ConfigError("channels carry no noise power; call compute_noise_power first")
+    if init is None:
+        init = init_precoders(config, project_sum_power)
+    v0 = init.precoders if isinstance(init, PrecoderSet) else np.asarray(init)
+    H = channels.channels
+    if H.shape != (config.K, config.N, config.M):
+        raise ConfigError(f"channels shape {H.shape} does not match config "
+                          f"(K={config.K}, N={config.N}, M={config.M})")
+    res = run_exact_batch(H[None].astype(np.complex128), channels.noise_power, config.p_max,
+                          config.weight_vector[None], v0[None].astype(np.complex128), options,
+                          record_trace=True)
+    raise_for_status(int(res.status[0]), gamma=0.0, omega=0.0)
+    return res.solve_result(0)
+
+
+def run_wmmse(channels: ChannelSet, config: SystemConfig, options: SolverOptions,
+              init=None) -> SolveResult:
+    """Exact block-coordinate WMMSE (ref solvers.py:521-527) on the device:
+    MMSE receivers, the standard weight update from t = 1, precoders by dual
+    bisection; stops on the relative WSR change."""
+    if options.algorithm is not Algorithm.WMMSE:
+        raise ConfigError("options.algorithm must be WMMSE")
+    return _run_exact(channels, config, options, init)
+
+
+def run_mmmse(channels: ChannelSet, config: SystemConfig, options: SolverOptions,
+              init=None) -> SolveResult:
+    """Two-stage warm-started exact solver (ref solvers.py:530-537): identity
+    weights until the relative WSR change first drops below eps1, then the
+    weighted updates until eps2."""
+    if options.algorithm is not Algorithm.MMMSE:
+        raise ConfigError("options.algorithm must be MMMSE")
+    return _run_exact(channels, config, options, init)
+
+
+_DRIVERS = {  # ref solvers.py:553-557
+    Algorithm.WMMSE: run_wmmse,
+    Algorithm.MMMSE: run_mmmse,
+    Algorithm.AMMMSE: run_ammmse,
+}
+
+
 def solve(channels: ChannelSet, config: SystemConfig, options: SolverOptions) -> SolveResult:
-    """Dispatch on options.algorithm (ref solvers.py:553-562).  Only A-MMMSE
-    runs on this engine; the exact drivers are out of scope."""
-    if options.algorithm is Algorithm.AMMMSE:
-        return run_ammmse(channels, config, options)
-    raise ConfigError(f"algorithm {options.algorithm.value!r} is not provided by the B200 engine "
-                      "(only A-MMMSE)")
+    """Dispatch on options.algorithm (ref solvers.py:553-562)."""
+    return _DRIVERS[options.algorithm](channels, config, options)

@@ -137,8 +137,12 @@ def lemma_bound_scan(H, noise_power, weights, bounds, U, W, V, iterations, t_chu
     eye = torch.eye(d, dtype=torch.complex128, device=dev)
     for t0 in range(0, T, t_chunk):
         t1 = min(T, t0 + t_chunk)
-        u, w, v = U[:, t0:t1], W[:, t0:t1], V[:, t0:t1]
         valid = (torch.arange(t0, t1, device=dev)[None, :] < iters[:, None])  # (B, t)
+        # iterates past a realization's last iteration are unwritten (NaN): zero them
+        keep = valid[:, :, None, None, None]
+        u = torch.where(keep, U[:, t0:t1], torch.zeros((), dtype=U.dtype, device=dev))
+        w = torch.where(keep, W[:, t0:t1], torch.zeros((), dtype=W.dtype, device=dev))
+        v = torch.where(keep, V[:, t0:t1], torch.zeros((), dtype=V.dtype, device=dev))
         # R[k, j] = U_k^H H_k V_j  (B, t, K, K, d, d)
         hv = torch.einsum("bknm,btjmd->btkjnd", H, v)
         R = torch.einsum("btkna,btkjnd->btkjad", u.conj(), hv)

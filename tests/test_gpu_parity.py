@@ -216,7 +216,7 @@ def test_cluster_streamed_odd_stage_rows_complex64(cuda):
         assert rel.max() <= WSR_RTOL_C64, (hp, rel)
 
 
-@pytest.mark.parametrize("M,K,N,d,csize", [(128, 16, 4, 4, 2), (256, 32, 2, 2, 4), (128, 32, 2, 2, 1),
+@pytest.mark.parametrize("M,K,N,d,csize", [(128, 16, 4, 4, 2), (256, 32, 2, 2, 4), (128, 32, 2, 2, 2),
                                            (128, 32, 4, 4, 4), (64, 16, 4, 4, 2)])
 def test_cluster_tensor_core_gemms_complex64(cuda, M, K, N, d, csize):
     """tcgen05 3xTF32 GEMMs (tensor_cores=1: bulk-copied pre-split H planes, TMEM

@@ -109,13 +109,21 @@ class TestErrors:
         with pytest.raises(UnstableParametersError, match="gamma"):
             raise_for_status(STATUS_UNSTABLE, gamma=1000.0, omega=0.9)
 
-    def test_solve_dispatch_rejects_other_algorithms(self):
+    def test_drivers_reject_other_algorithms(self):
+        # each driver checks its algorithm before any device work (solvers.py:524-548)
         cfg = pkg.SystemConfig(M=4, N=1, K=1, d=1)
         ch = pkg.ChannelSet(np.ones((1, 1, 4)), noise_power=1.0)
         with pytest.raises(ConfigError):
-            pkg.solve(ch, cfg, pkg.SolverOptions(algorithm="wmmse"))
-        with pytest.raises(ConfigError):
             pkg.run_ammmse(ch, cfg, pkg.SolverOptions(algorithm="mmmse"))
+        with pytest.raises(ConfigError):
+            pkg.run_wmmse(ch, cfg, pkg.SolverOptions(algorithm="ammmse"))
+        with pytest.raises(ConfigError):
+            pkg.run_mmmse(ch, cfg, pkg.SolverOptions(algorithm="wmmse"))
+        from paper_2510_20507_b200.solvers import _DRIVERS
+
+        assert _DRIVERS[pkg.Algorithm.WMMSE] is pkg.run_wmmse
+        assert _DRIVERS[pkg.Algorithm.MMMSE] is pkg.run_mmmse
+        assert _DRIVERS[pkg.Algorithm.AMMMSE] is pkg.run_ammmse
 
 
 def _declared_functions(header):
