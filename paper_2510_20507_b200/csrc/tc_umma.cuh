@@ -169,12 +169,16 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// tf32 split: hi = x rounded to tf32 (ties away, cvt.rna), lo = x - hi (exact in fp32)
+// tf32 split: hi = x rounded to tf32 (ties away, cvt.rna), lo = x - hi (exact
+// in fp32) rounded to tf32 as well: the tensor core reads only the top 19
+// bits of an operand, so an unrounded lo would be truncated (biased, 2^-21
+// relative) instead of rounded (2^-22)
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
+  uint32_t h, l;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
   hi = __uint_as_float(h);
-  lo = x - hi;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
 }
 
 }  // namespace umma

@@ -61,5 +61,10 @@ def test_tc_gemm_matches_complex128(cuda, gslib, KN, M, ncol, mode):
     ref = H64 @ B64 if mode % 2 == 0 else np.conj(np.swapaxes(H64, 1, 2)) @ B64
     scale = np.sqrt(kd)  # |entries| ~ sqrt(kd)
     err = np.abs(got - ref).max() / scale
+    # fp32 FFMA-class reference: the same product in complex64 numpy (BLAS fp32)
+    H32, B32 = H, B
+    f32 = H32 @ B32 if mode % 2 == 0 else np.conj(np.swapaxes(H32, 1, 2)) @ B32
+    err32 = np.abs(f32.astype(np.complex128) - ref).max() / scale
+    print(f"KN={KN} M={M} ncol={ncol} mode={mode}: 3xTF32 err {err:.2e}, fp32 BLAS err {err32:.2e}")
     assert np.isfinite(got).all()
-    assert err < 1e-5, err
+    assert err < 4 * err32 + 1e-7, (err, err32)
