@@ -47,7 +47,24 @@ $(PHASES_LIB): $(PHASES_OBJS)
 
 phases: $(PHASES_LIB)
 
-clean:
-	rm -rf build $(LIB) $(PROBE) $(TCTEST) $(GEMMSTEP) $(PHASES_LIB)
+# development library: only the float N = d = 4 cluster kernels (BASELINE large),
+# one translation unit; load it with AMMMSE_LIB=paper_2510_20507_b200/libammmse_dev.so
+DEV_OBJ := build/obj_dev
+DEV_LIB := paper_2510_20507_b200/libammmse_dev.so
+DEV_SRCS := $(SRC_DIR)/ammmse_capi.cu $(SRC_DIR)/ammmse_gen.cu $(SRC_DIR)/exact_engine.cu $(SRC_DIR)/tools/dev_inst.cu
+DEV_OBJS := $(patsubst $(SRC_DIR)/%.cu,$(DEV_OBJ)/%.o,$(DEV_SRCS))
+DEVFLAGS ?=
 
-.PHONY: all clean phases
+$(DEV_OBJ)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v -DAMMMSE_PHASES=$(PHASES) $(DEVFLAGS) -c $< -o $@ > $@.ptxas.log 2>&1 || (cat $@.ptxas.log; exit 1)
+
+$(DEV_LIB): $(DEV_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(DEV_OBJS)
+
+dev: $(DEV_LIB)
+
+clean:
+	rm -rf build $(LIB) $(PROBE) $(TCTEST) $(GEMMSTEP) $(PHASES_LIB) $(DEV_LIB)
+
+.PHONY: all clean phases dev
