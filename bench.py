@@ -521,10 +521,10 @@ def main():
         eng.solve(dH, ds2, dP, dA, dV0, out=res, stream=stream, **kw)
         torch.cuda.synchronize()
         del os.environ["AMMMSE_PROFILE_PHASES"]
-        sh = (ctypes.c_double * 16)()
+        sh = (ctypes.c_double * 32)()
         f0, nb = ctypes.c_int(), ctypes.c_int()
         ws = eng._workspace(0, stream)
-        n = _native.lib().ammmse_phase_profile(ws.data_ptr(), sh, 16, ctypes.byref(f0),
+        n = _native.lib().ammmse_phase_profile(ws.data_ptr(), sh, 32, ctypes.byref(f0),
                                                ctypes.byref(nb), stream.cuda_stream)
         if n > 0:
             share = sum(sh[f0.value + i] for i in range(nb.value))

@@ -1,0 +1,4 @@
+export PATH=/usr/local/cuda/bin:$PATH
+export PYTHONPATH=$PWD
+export AMMMSE_LIB=paper_2510_20507_b200/libammmse_dev.so
+timeout 300 python exp/s4_tc2.py 64 > gpurun_out/s4_tc2_cmp.log 2>&1; tail -32 gpurun_out/s4_tc2_cmp.log

@@ -13,7 +13,7 @@
 #include <string.h>
 
 #include "ammmse.h"
-#include "ammmse_cluster.cuh"
+#include "ammmse_tc2.cuh"
 #include "entries.h"
 
 namespace {
@@ -23,7 +23,7 @@ thread_local char g_err[256];  // per-thread text of the last error (ammmse_erro
 // workspace layout: [0, 8) persistent-kernel work counter, [64, 192) phase
 // counters (diagnostic builds), scratch from byte 256
 constexpr size_t kPhaseOff = 64;
-constexpr int kPhaseN = 10;
+constexpr int kPhaseN = 20;
 
 const ammmse::KernelEntry* lookup(const AmmmseDims* d) {
   if (d->N < 1 || d->N > 4 || d->d < 1 || d->d > 4) return nullptr;
@@ -69,7 +69,8 @@ struct Plan {
   int hres;     // cluster engine: H resident (1) or streamed (0)
   int vglob;    // cluster engine: V_old in global scratch
   int sb;       // cluster engine: staging bytes per buffer
-  int tc;       // cluster engine: tcgen05 GEMMs
+  int tc;       // cluster engine: tcgen05 GEMMs (1: ammmse_cluster_kernel<TC>, 2: ammmse_tc2_kernel)
+  int stages;   // tc == 2: A ring depth
   size_t smem;
   int threads;
 };
@@ -86,6 +87,7 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_core
   p->vglob = 0;
   p->sb = 20480;
   p->tc = 0;
+  p->stages = 0;
   if (force_c == 0 && h_placement == 0 && tensor_cores != 1) {
     const size_t s1 = e->smem_bytes(d->M, d->K);
     if (s1 <= (size_t)lim) {
@@ -120,6 +122,26 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_core
       // 0.4 of the FMA peak while the per-chunk handoffs of the tensor-core
       // ring are latency bound, bench_gemmstep.py).
       const int ncol = (d->K / c) * d->d;
+      // second-generation tensor-core engine (ammmse_tc2.cuh: split operands
+      // resident, precoders in TMEM, one-thread A ring with cross-GEMM
+      // prefetch): tensor_cores = 3, or automatically for N = d = 4
+      if (mi == 0 && d->dtype == AMMMSE_COMPLEX64 && e->cluster_solve_tc2 && h_placement == 0 &&
+          (tensor_cores == 3 || (tensor_cores == 0 && d->N == 4 && d->d == 4)) &&
+          ammmse::tc2::shape_ok(d->M, d->K * d->N, ncol)) {
+        const int st = e->tc2_stages(d->M, d->K, c, (size_t)lim - 256);  // static shared: ctl, mbarriers
+        if (st >= 2) {
+          p->cluster = c;
+          p->hres = 0;
+          p->vglob = 0;
+          p->sb = 0;
+          p->tc = 2;
+          p->stages = st;
+          p->smem = e->tc2_smem_bytes(d->M, d->K, c, st);
+          p->threads = 256;
+          return AMMMSE_OK;
+        }
+      }
+      if (tensor_cores == 3) continue;
       const bool tc_auto = tensor_cores == 0 && d->N == 4 && d->d == 4;
       if (!hres && d->dtype == AMMMSE_COMPLEX64 && (tensor_cores == 1 || tc_auto) &&
           ammmse::tc_shape_ok(d->M, d->K * d->N, ncol)) {
@@ -263,7 +285,7 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   }
   Plan plan;
   if (opt->cluster_size < 0 || opt->h_placement < 0 || opt->h_placement > 3 ||
-      opt->tensor_cores < 0 || opt->tensor_cores > 2 ||
+      opt->tensor_cores < 0 || opt->tensor_cores > 3 ||
       make_plan(dims, opt->cluster_size, opt->h_placement, opt->tensor_cores, &plan) != AMMMSE_OK) {
     snprintf(g_err, sizeof g_err, "no engine configuration fits (cluster_size %d)", opt->cluster_size);
     return AMMMSE_ERR_UNSUPPORTED;
@@ -272,7 +294,9 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
     snprintf(g_err, sizeof g_err, "workspace missing or too small");
     return AMMMSE_ERR_WORKSPACE;
   }
-  const void* func = plan.cluster ? (plan.tc ? plan.e->cluster_solve_tc : plan.e->cluster_solve)
+  const void* func = plan.cluster ? (plan.tc == 2   ? plan.e->cluster_solve_tc2
+                                     : plan.tc ? plan.e->cluster_solve_tc
+                                               : plan.e->cluster_solve)
                                   : plan.e->solve;
   {  // shape-specialised single-CTA kernel (AMMMSE_NO_SPEC=1 disables it, for A/B)
     const char* ns = getenv("AMMMSE_NO_SPEC");
@@ -392,6 +416,7 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.sb_bytes = plan.sb;
   a.scratch = reinterpret_cast<unsigned char*>(workspace) + 256;
   a.tcm = plan.cluster ? plan.tc : 0;
+  a.tc_stages = plan.stages;
   if (a.tcm) {  // H planes after the V_old slots, 256-byte aligned
     int sms2 = 0;
     cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);
@@ -404,6 +429,8 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   // diagnostic builds (AMMMSE_PHASES=1) with AMMMSE_PROFILE_PHASES=1: per-phase
   // thread-0 clock64 totals into the caller's workspace (ammmse_phase_profile)
   if (AMMMSE_PHASES) {
+    const char* de = getenv("AMMMSE_DBG");
+    a.dbg = de ? atoi(de) : 0;
     const char* pe = getenv("AMMMSE_PROFILE_PHASES");
     if (pe && pe[0] == '1') {
       a.prof = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(workspace) + kPhaseOff);

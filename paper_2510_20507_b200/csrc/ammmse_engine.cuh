@@ -86,6 +86,8 @@ struct EngineArgs {
   unsigned char* scratch;  // cluster engine: per-CTA global scratch (vold_glob)
   int tcm;                 // cluster engine: tcgen05 3xTF32 GEMMs (streamed H planes)
   float* hplanes;          // tcm: per-cluster pre-split H planes (8 x KN x M floats each)
+  int tc_stages;           // tcm == 2 (ammmse_tc2.cuh): A ring depth
+  int dbg;                 // diagnostic builds: ablation bits (AMMMSE_DBG)
   unsigned long long* prof;  // debug: per-phase clock64 totals (nullptr = off)
   long long B;
   unsigned long long* counter;
@@ -145,7 +147,7 @@ struct Layout {
 // Debug phase timers: thread 0 of every CTA accumulates clock64() deltas per
 // phase and adds them to EngineArgs::prof at exit (built with AMMMSE_PHASES=1 and run
 // with AMMMSE_PROFILE_PHASES=1; the counters live in the caller's workspace).
-constexpr int kProfPhases = 10;
+constexpr int kProfPhases = 20;
 #ifndef AMMMSE_PHASES
 #define AMMMSE_PHASES 0  // compile-time switch: production kernels carry no timers
 #endif
@@ -168,6 +170,11 @@ struct PhaseClock {
       last = now;
     }
   }
+  // fine-grained marks inside single-thread role loops: AMMMSE_PHASES=2 only
+  // (they lengthen the loops they measure)
+  __device__ __forceinline__ void mark2(int i) {
+    if (AMMMSE_PHASES >= 2) mark(i);
+  }
   __device__ void flush() {
     if (out)
       for (int i = 0; i < kProfPhases; ++i) atomicAdd(out + i, (unsigned long long)acc[i]);
@@ -177,6 +184,7 @@ struct PhaseClock {
 struct PhaseClock {
   __device__ __forceinline__ void init(unsigned long long*) {}
   __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void mark2(int) {}
   __device__ __forceinline__ void flush() {}
 };
 #endif

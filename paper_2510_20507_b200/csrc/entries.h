@@ -21,6 +21,10 @@ struct KernelEntry {
   int n_solve_specs = 0;
   const SpecEntry* cluster_specs = nullptr;    // FFMA cluster kernels for fixed (M, K, C), T = 256
   int n_cluster_specs = 0;
+  // second-generation tensor-core cluster engine (ammmse_tc2.cuh; float only)
+  const void* cluster_solve_tc2 = nullptr;     // ammmse_tc2_kernel<N, d>
+  int (*tc2_stages)(int M, int K, int C, size_t limit) = nullptr;   // A ring depth that fits (0: none)
+  size_t (*tc2_smem_bytes)(int M, int K, int C, int stages) = nullptr;
 };
 
 // entries_<real>_<N>()[d - 1], d = 1..4

@@ -86,6 +86,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       : "memory");
 }
 
+// Busy-poll variant (mbarrier.test_wait, no hardware suspend): for the single
+// role threads of a pipeline, whose handoff latency is on the critical path.
+// try_wait may park the thread for a system-dependent time slice; measured on
+// B200, a try_wait handoff costs ~1 k cycles per hop.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* mbar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(mbar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
 }
