@@ -36,8 +36,13 @@ namespace tc2 {
 
 constexpr int KW = 8;          // K per chunk = one tf32 UMMA K-step
 constexpr int kPerm = 3;       // permanent A ring stages (they also hold the chunks prefetched across GEMMs)
-constexpr int kVol = 4;        // volatile stages: the two G buffers (dead during the MMA loops), 2 each
-constexpr int kStages = kPerm + kVol;  // compile time: the MMA loop is unrolled by stage
+constexpr int kVol = 3;        // volatile stages in the two G buffers (dead during the MMA loops): 2 + 1
+// An EVEN number of stages: chunk c uses stage c % kStages, so the chunks of even
+// and of odd index (two producer / MMA warp pairs, see gemm) never share a stage
+// and each pair is an in-order pipeline of its own.  (With 7 stages a warp could
+// poll a barrier two phases ahead of a lagging pair: parity aliasing.)
+constexpr int kStages = kPerm + kVol;
+static_assert(kStages % 2 == 0, "even / odd chunk pipelines must not share stages");
 constexpr int kMaxStages = kStages;
 constexpr int kBPad = 32;      // bytes between B chunks (bank spread of the per-row epilogue stores)
 constexpr int kThreads = 256;
@@ -244,8 +249,8 @@ struct Pipe {
   int dbg = 0;  // diagnostics (AMMMSE_PHASES builds): bit 0 skips the A copies, bit 1 the MMAs
 };
 
-constexpr int kMmaWarp = 0;
-constexpr int kProducerWarp = 1;
+constexpr int kMmaWarp = 0, kMmaWarp2 = 2;  // (different SM sub-partitions)
+constexpr int kProducerWarp = 1, kProducerWarp2 = 3;
 
 // D = A · B over nch chunks of K (all threads call).  A = planes Ag of 128
 // rows; B = the split operand in p.bfull (ncol columns); accumulators of set s at
@@ -273,33 +278,46 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
   const uint32_t have = p.have;
   const uint32_t npf = next_Ag ? (uint32_t)kPerm : 0u;
   const int warp = threadIdx.x >> 5;
-  if (warp == kProducerWarp) {
-    const uint32_t ring0 = umma::smem_u32(p.ring), vol0 = umma::smem_u32(p.vol0),
-                   vol1 = umma::smem_u32(p.vol1), full0 = umma::smem_u32(p.full),
-                   done0 = umma::smem_u32(p.done);
+  // Two producer warps (chunks of even / odd index) and, with two accumulator
+  // sets, two MMA warps (even chunks -> set 0, odd chunks -> set 1; MMAs of
+  // different threads are unordered, so each warp owns its accumulators): the
+  // ~450 cycles a role warp spends per chunk on barrier operations overlap.
+  // Every warp walks ALL chunks to keep the per-stage phase masks current and
+  // acts on its own.
+  const int nmw = (nsets == 2 && !(AMMMSE_PHASES && (p.dbg & 8))) ? 2 : 1;
+  const bool one_producer = AMMMSE_PHASES && (p.dbg & 16);
+  const uint32_t stage_base0 = umma::smem_u32(p.ring), stage_base1 = umma::smem_u32(p.vol0),
+                 stage_base2 = umma::smem_u32(p.vol1), full0 = umma::smem_u32(p.full),
+                 done0 = umma::smem_u32(p.done);
+  auto stage_addr = [&](uint32_t s) {
+    return s < (uint32_t)kPerm       ? stage_base0 + s * a_bytes
+           : s < (uint32_t)kPerm + 2 ? stage_base1 + (s - kPerm) * a_bytes
+                                     : stage_base2 + (s - kPerm - 2) * a_bytes;
+  };
+  if (warp == kProducerWarp || warp == kProducerWarp2) {
+    const uint32_t me = warp == kProducerWarp ? 0u : 1u;
     const bool nocopy = AMMMSE_PHASES && (p.dbg & 1);
     uint32_t pm = p.pm, ever = p.ever;
-    auto fill = [&](uint32_t s, const unsigned char* src) {
+    auto fill = [&](uint32_t c, uint32_t s, const unsigned char* src) {
       const uint32_t bit = 1u << s;
-      const uint32_t fb = full0 + 8u * s, db = done0 + 8u * s;
-      const uint32_t dst = s < (uint32_t)kPerm       ? ring0 + s * a_bytes
-                           : s < (uint32_t)kPerm + 2 ? vol0 + (s - kPerm) * a_bytes
-                                                     : vol1 + (s - kPerm - 2) * a_bytes;
-      // the stage's previous MMAs completed (done completion number fills - 1)
-      if (ever & bit) mbar_wait_spin_u32(db, ((pm >> s) & 1u) ^ 1u);
-      if (nocopy) {
-        if (elect_one()) mbar_arrive_u32(fb);
-      } else {
-        // copy first: its latency is the long pole; the phase cannot complete
-        // before the arrive, whatever the order of complete_tx / expect_tx
-        asm volatile(
-            "{\n\t.reg .pred Pe;\n\t"
-            "elect.sync _|Pe, 0xffffffff;\n\t"
-            "@Pe cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
-            "@Pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
-            "}\n" ::"r"(dst),
-            "l"(src), "r"(a_bytes), "r"(fb)
-            : "memory");
+      if (one_producer ? me == 0u : (c & 1u) == me) {
+        const uint32_t fb = full0 + 8u * s, db = done0 + 8u * s, dst = stage_addr(s);
+        // the stage's previous MMAs completed (done completion number fills - 1)
+        if (ever & bit) mbar_wait_spin_u32(db, ((pm >> s) & 1u) ^ 1u);
+        if (nocopy) {
+          if (elect_one()) mbar_arrive_u32(fb);
+        } else {
+          // copy first: its latency is the long pole; the phase cannot complete
+          // before the arrive, whatever the order of complete_tx / expect_tx
+          asm volatile(
+              "{\n\t.reg .pred Pe;\n\t"
+              "elect.sync _|Pe, 0xffffffff;\n\t"
+              "@Pe cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t"
+              "@Pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+              "}\n" ::"r"(dst),
+              "l"(src), "r"(a_bytes), "r"(fb)
+              : "memory");
+        }
       }
       pm ^= bit;
       ever |= bit;
@@ -307,18 +325,16 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
     const unsigned char* src = reinterpret_cast<const unsigned char*>(Ag) + (size_t)have * a_bytes;
     uint32_t s = have % kStages;
     for (uint32_t c = have; c < (uint32_t)nch; ++c, src += a_bytes) {
-      fill(s, src);
+      fill(c, s, src);
       if (++s == (uint32_t)kStages) s = 0;
     }
     src = reinterpret_cast<const unsigned char*>(next_Ag);
-    for (uint32_t c = 0; c < npf; ++c, src += a_bytes) fill(c, src);
+    for (uint32_t c = 0; c < npf; ++c, src += a_bytes) fill(c, c, src);
     p.pm = pm;
     p.ever = ever;
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp || warp == kMmaWarp2) {
+    const uint32_t me = warp == kMmaWarp ? 0u : 1u;
     const uint32_t idesc = umma::make_idesc_tf32(128, 2 * ncol, false, false, false, false);
-    const uint32_t ring0 = umma::smem_u32(p.ring), vol0 = umma::smem_u32(p.vol0),
-                   vol1 = umma::smem_u32(p.vol1), full0 = umma::smem_u32(p.full),
-                   done0 = umma::smem_u32(p.done);
     // descriptors: the start address (>> 4, 14 bits: a CTA of a cluster sees its
     // shared window at a rank-dependent base, so the field is masked) is the low
     // word's low bits; the high word is constant
@@ -332,55 +348,47 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
     const uint32_t tmem = p.tmem;
     const bool nomma = AMMMSE_PHASES && (p.dbg & 2);
     uint32_t cm = p.cm;
-    uint32_t ok = mbar_test_u32(full0, cm & 1u);  // stage 0
-    int c = 0;
-    // one stage-specialised body: `i` is a compile-time stage index
-    auto body = [&](auto stage_c) {
-      constexpr int i = decltype(stage_c)::value;
-      constexpr int nx = (i + 1) % kStages;
-      const uint32_t fb = full0 + 8u * i;
-      const uint32_t par = (cm >> i) & 1u;
-      // (no tcgen05 fence: the operands arrive through the async proxy, whose
-      // complete_tx on the barrier is what the MMA's own async reads are ordered by)
-      while (!ok) ok = mbar_test_u32(fb, par);
-      cm ^= 1u << i;
-      pc.mark2(16);  // (AMMMSE_PHASES=2) MMA warp: waiting for A chunks
-      const uint32_t abase = i < kPerm       ? ring0 + (uint32_t)i * a_bytes
-                             : i < kPerm + 2 ? vol0 + (uint32_t)(i - kPerm) * a_bytes
-                                             : vol1 + (uint32_t)(i - kPerm - 2) * a_bytes;
-      const uint32_t al = dlo | lo14(abase);
-      // The chunk's six MMAs and the poll of the NEXT stage's barrier in one asm
-      // block: the poll is issued first and its predicate is consumed after the
-      // MMAs, so its ~100-cycle round trip hides behind them (with 7 stages the
-      // next chunk has normally landed).
-      const bool last = c + 1 >= nch;
-      const uint32_t nfb = last ? fb : full0 + 8u * nx;
-      const uint32_t npar = last ? par : (cm >> nx) & 1u;
-      const uint64_t bhi = dhi | b_lo, blo = dhi | (b_lo + lo_off);
-      const int set = nsets == 2 ? (c & 1) : 0;
-      const uint32_t acc = c >= nsets ? 1u : 0u;
-      const uint32_t d1 = tmem + (uint32_t)(set * 4 * ncol);
-      const uint32_t d2 = d1 + (uint32_t)(2 * ncol);
-      ok = mma6_poll(d1, d2, dhi | al, dhi | (al + pl), dhi | (al + 2 * pl), dhi | (al + 3 * pl), bhi, blo,
-                     idesc, acc, nfb, npar, nomma ? 0u : 1u, done0 + 8u * i);
-      if (last) ok = 0u;
-      pc.mark2(17);  // issuing
-      b_lo += b_inc;
-      ++c;
-    };
-    static_assert(kStages == 7, "the stage dispatch below is written for 7 stages");
-    while (c < nch) {
-      body(std::integral_constant<int, 0>{});
-      if (c < nch) body(std::integral_constant<int, 1>{});
-      if (c < nch) body(std::integral_constant<int, 2>{});
-      if (c < nch) body(std::integral_constant<int, 3>{});
-      if (c < nch) body(std::integral_constant<int, 4>{});
-      if (c < nch) body(std::integral_constant<int, 5>{});
-      if (c < nch) body(std::integral_constant<int, 6>{});
+    const bool active = (int)me < nmw;
+    // first own chunk: me (stage me)
+    uint32_t ok = active && (int)me < nch ? mbar_test_u32(full0 + 8u * me, (cm >> me) & 1u) : 0u;
+    uint32_t s = 0;
+    for (int c = 0; c < nch; ++c, b_lo += b_inc) {
+      const uint32_t bit = 1u << s;
+      if (active && ((uint32_t)c & (uint32_t)(nmw - 1)) == me) {
+        const uint32_t fb = full0 + 8u * s;
+        const uint32_t par = (cm >> s) & 1u;
+        // (no tcgen05 fence: the operands arrive through the async proxy, whose
+        // complete_tx on the barrier is what the MMA's own async reads are ordered by)
+        while (!ok) ok = mbar_test_u32(fb, par);
+        pc.mark2(16);  // (AMMMSE_PHASES=2) MMA warp: waiting for A chunks
+        const uint32_t al = dlo | lo14(stage_addr(s));
+        // The chunk's six MMAs, its commit and the poll of this warp's NEXT chunk's
+        // barrier in one asm block: the poll is issued first and its predicate is
+        // consumed last, so its round trip hides behind the rest.
+        const int cn = c + nmw;
+        const bool last = cn >= nch;
+        uint32_t s2 = s + (uint32_t)nmw;
+        if (s2 >= (uint32_t)kStages) s2 -= kStages;
+        const uint32_t nfb = last ? fb : full0 + 8u * s2;
+        const uint32_t npar = last ? par : (cm >> s2) & 1u;
+        const uint64_t bhi = dhi | b_lo, blo = dhi | (b_lo + lo_off);
+        const int set = nsets == 2 ? (c & 1) : 0;
+        const uint32_t acc = c >= nsets ? 1u : 0u;
+        const uint32_t d1 = tmem + (uint32_t)(set * 4 * ncol);
+        const uint32_t d2 = d1 + (uint32_t)(2 * ncol);
+        ok = mma6_poll(d1, d2, dhi | al, dhi | (al + pl), dhi | (al + 2 * pl), dhi | (al + 3 * pl), bhi,
+                       blo, idesc, acc, nfb, npar, nomma ? 0u : 1u, done0 + 8u * s);
+        if (last) ok = 0u;
+        pc.mark2(17);  // issuing
+      }
+      cm ^= bit;
+      if (++s == (uint32_t)kStages) s = 0;
     }
-    if (elect_one()) umma::commit(p.fin);
-    __syncwarp();
-    umma::mbar_wait_spin(p.fin, p.call & 1u);  // all MMAs of this call completed
+    if (active) {
+      if (elect_one()) umma::commit(p.fin);  // fin counts one arrival per MMA warp
+      __syncwarp();
+    }
+    if (warp == kMmaWarp) umma::mbar_wait_spin(p.fin, p.call & 1u);  // all MMAs of this call completed
     pc.mark2(18);  // tail: the last MMAs
     p.cm = cm;
   }
@@ -393,13 +401,13 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
 // Consume prefetched chunks that no GEMM will use (end of a realization): wait
 // for each copy to land, then release its stage.
 __device__ __forceinline__ void drain(Pipe& p) {
-  if ((threadIdx.x >> 5) == kMmaWarp) {
-    for (uint32_t s = 0; s < p.have; ++s) {
+  for (uint32_t s = 0; s < p.have; ++s) {
+    if ((threadIdx.x >> 5) == kMmaWarp) {
       mbar_wait_spin_u32(umma::smem_u32(p.full) + 8u * s, (p.cm >> s) & 1u);
-      p.cm ^= 1u << s;
       if (elect_one()) mbar_arrive_u32(umma::smem_u32(p.done) + 8u * s);
       __syncwarp();
     }
+    p.cm ^= 1u << s;  // (every warp keeps its copy of the phase mask current)
   }
   p.have = 0;
 }
@@ -449,6 +457,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
   __shared__ unsigned long long s_r;
   __shared__ uint64_t tc_full[tc2::kMaxStages], tc_done[tc2::kMaxStages], tc_fin;
   __shared__ uint32_t tc_tmem_slot;
+  __shared__ double xl[16 * 8];  // local copy of every CTA's exchange slots 0..7 (xs_fetch)
+  __shared__ double s_power;     // cluster ‖X‖² of the iteration
   __builtin_assume(blockDim.x == tc2::kThreads);
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       umma::mbar_init(&tc_full[q], 1);
       umma::mbar_init(&tc_done[q], 1);
     }
-    umma::mbar_init(&tc_fin, 1);
+    umma::mbar_init(&tc_fin, (L.nsets == 2 && !(AMMMSE_PHASES && (a.dbg & 8))) ? 2 : 1);  // one commit per MMA warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc<512>(&tc_tmem_slot);  // one CTA per SM (shared-memory size)
@@ -552,6 +562,40 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     double s = 0.0;
     for (int c = 0; c < C; ++c) s += cl.map_shared_rank(xs, c)[sl];
     return s;
+  };
+  // Batched read of the cluster's exchange slots 0..7 by warp 0 (one DSMEM
+  // round trip instead of a dozen dependent ones on thread 0); the fixed-order
+  // sums below then run on local shared memory.  Call after the cluster
+  // barrier that publishes the slots; only warp 0 may use xlsum / xlfirst.
+  auto xs_fetch = [&]() {
+    if (warp == 0) {
+      for (int i = lane; i < C * 8; i += 32) xl[i] = cl.map_shared_rank(xs, i >> 3)[i & 7];
+      __syncwarp();
+    }
+  };
+  auto xlsum = [&](int sl) {
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += xl[c * 8 + sl];
+    return s;
+  };
+  auto xlfirst = [&](int sl) {
+    for (int c = 0; c < C; ++c) {
+      const double v = xl[c * 8 + sl];
+      if (v != 0.0) return (int)v;
+    }
+    return 0;
+  };
+  // cluster sum of slot sl to every thread of the block: warp 0 reads the C
+  // remote values in parallel, fixed-order sum, broadcast through shared memory
+  auto xsum_block = [&](int sl) {
+    if (warp == 0) {
+      const double v = lane < C ? cl.map_shared_rank(xs, lane)[sl] : 0.0;
+      double s = 0.0;
+      for (int c = 0; c < C; ++c) s += __shfl_sync(0xffffffffu, v, c);
+      if (lane == 0) s_power = s;
+    }
+    __syncthreads();
+    return s_power;
   };
   auto xfirst = [&](int sl) {
     for (int c = 0; c < C; ++c) {
@@ -723,78 +767,14 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       // four lanes per user (user_algebra_quad.cuh)
       if (warp != 1 && warp != 2) return;
       if (warp == 2 && !weighted) return;
-      const int ul = lane >> 2, sc = lane & 3;
-      for (int kl0 = 0; kl0 < KL; kl0 += 8) {
-        const bool act = kl0 + ul < KL;
-        const int kl = act ? kl0 + ul : 0;
-        cd Tg[4][4], Gkk[4][4], gs[4];
-        k1_load(gsrc, kl, Tg, Gkk);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // column sc of the diagonal block (no dynamic register indexing)
-          const int idx = ((k0 + kl) * 4 + q) * ldg + kl * 4 + sc;
-          gs[q] = cmk((double)Gr[gsrc][idx], (double)Gi[gsrc][idx]);
-        }
-        double* scr = k1w + (size_t)kl * quad::kScratch;
-        cd* yscr = reinterpret_cast<cd*>(scr);
-        cd* pscr = reinterpret_cast<cd*>(scr + 32);
-        double* pvc = scr + 64;
-        cd* ucol = ucb[bout] + (size_t)kl * 16;
-        cd* wcol = wcb[bout] + (size_t)kl * 16;
-        if (warp == 2) {
-          double pivc[4];
-          int pd;
-          quad::k1w_quad(Tg, Gkk, gs, ctl.sigma2, sc, yscr, wcol, pivc, pd);
-          if (sc == 0) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) pvc[j] = pivc[j];
-            pvc[4] = (double)pd;
-          }
-          asm volatile("bar.sync 1, 64;\n" ::: "memory");
-        } else {
-          cd Wprow[4], Ufull[4][4], us[4], tcol[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) Wprow[q] = wcb[bin][(size_t)kl * 16 + sc * 4 + q];
-          double fu_, nT, piva[4];
-          int st;
-          quad::k1u_quad(Tg, gs, ctl.sigma2, alpha[kl], Wprow, lndb[bin][kl], sc, ucol, Ufull, us, tcol, fu_,
-                         nT, piva, st);
-          cd wcs[4];
-          double pivc[4] = {1.0, 1.0, 1.0, 1.0};
-          int pdc = 1;
-          if (weighted) {
-            asm volatile("bar.sync 1, 64;\n" ::: "memory");
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              wcs[q] = wcol[q * 4 + sc];
-              pivc[q] = pvc[q];
-            }
-            pdc = (int)pvc[4];
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) wcs[q] = cmk(q == sc ? 1.0 : 0.0);
-          }
-          cd pcol[4], dcol[4];
-          double fw_, lnw;
-          quad::k1c_quad(Ufull, us, tcol, nT, piva, wcs, pivc, pdc, alpha[kl], weighted, sc, pscr, pcol, dcol,
-                         fw_, lnw, st);
-          if (act) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // row q, column sc
-              const int ig = ((k0 + kl) * 4 + q) * 4 + sc, il = (kl * 4 + q) * 4 + sc;
-              Uall[ig] = RC<R>{(R)us[q].r, (R)us[q].i};
-              Pall[ig] = RC<R>{(R)pcol[q].r, (R)pcol[q].i};
-              Down[il] = RC<R>{(R)dcol[q].r, (R)dcol[q].i};
-              if (!weighted) wcol[q * 4 + sc] = wcs[q];
-            }
-            if (sc == 0) {
-              lndb[bout][kl] = lnw;
-              fu[kl] = fu_;
-              fw[kl] = fw_;
-              ust[kl] = st;
-            }
-          }
-        }
-      }
+      const quad::QuadArgs qa{Gr[gsrc], Gi[gsrc], ldg, k0, KL, gx[0], ctl.sigma2, alpha};
+      const quad::K1Out4 ko{ucb[bout], wcb[bout], lndb[bout], fu, fw, ust,
+                            reinterpret_cast<float2*>(Uall), reinterpret_cast<float2*>(Pall),
+                            reinterpret_cast<float2*>(Down), k1w};
+      if (warp == 2)
+        quad::k1_weight_users(qa, ko);
+      else
+        quad::k1_recv_users(qa, ko, wcb[bin], lndb[bin], weighted);
       return;
     }
     constexpr bool closed = NN == 2 && DD == 2;
@@ -877,6 +857,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     __syncthreads();
     if (tid == 0) k1_publish();
     cl.sync();
+    xs_fetch();
     k1_gather();
   };
 
@@ -1238,9 +1219,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     for (int t = 1; t <= a.max_iters; ++t) {
       const int bk = t & 1;  // bank holding K1(t)'s U / W / ln det W
       if (tid == 0) {        // K1(t) results (published before the last cluster barrier)
-        ctl.f_u = xsum(XS_FU);
-        ctl.f_w = xsum(XS_FW);
-        const int st = xfirst(XS_ST1);
+        ctl.f_u = xlsum(XS_FU);  // (local copies: xs_fetch after the publishing barrier)
+        ctl.f_w = xlsum(XS_FW);
+        const int st = xlfirst(XS_ST1);
         if (st) {  // update_weight_matrices raised inside iteration t (solvers.py:455-460)
           if (!ctl.latched && wn) {
             if (a.latch) ctl.latched = 1;
@@ -1270,7 +1251,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       // G' = H X_new while the cluster sums ‖X_new‖² (the projection scale is lazy)
       tc2::gemm(pipe, pc, hpB, nchB, ncol, nsets, hpA);
       asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      const double power = xsum(XS_POWER);
+      const double power = xsum_block(XS_POWER);
       double scale = 1.0;
       if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);  // project_sum_power :257-263
       if (xo) vs1 = (float)scale; else vs0 = (float)scale;
@@ -1297,38 +1278,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
         const cd* ucache = ucb[bk];
         const cd* wcache = wcb[bk];
         if constexpr (NN == 4 && DD == 4) {  // four lanes per user (user_algebra_quad.cuh)
-          const int ul = lane >> 2, sc = lane & 3;
-          for (int kl0 = 0; kl0 < KL; kl0 += 8) {
-            const bool act = kl0 + ul < KL;
-            const int kl = act ? kl0 + ul : 0;
-            cd Tg[4][4], Gkk[4][4], U[4][4];
-            gram_of(1, kl, Tg);
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int idx = ((k0 + kl) * 4 + p) * ldg + kl * 4 + q;
-                Gkk[p][q] = cmk((double)Gr[GN][idx], (double)Gi[GN][idx]);
-                U[p][q] = ucache[(kl * 4 + p) * 4 + q];
-              }
-            cd gs[4], us[4], ws[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {  // column sc (no dynamic register indexing)
-              const int idx = ((k0 + kl) * 4 + q) * ldg + kl * 4 + sc;
-              gs[q] = cmk((double)Gr[GN][idx], (double)Gi[GN][idx]);
-              us[q] = ucache[(kl * 4 + q) * 4 + sc];
-              ws[q] = wcache[(kl * 4 + q) * 4 + sc];
-            }
-            const double wss = wcache[(kl * 4 + sc) * 4 + sc].r;
-            double rr, ff;
-            int st;
-            quad::wsr_quad(Tg, Gkk, gs, ctl.sigma2, alpha[kl], U, us, ws, wss, lndb[bk][kl], sc, rr, ff, st);
-            if (act && sc == 0) {
-              rate[kl] = rr;
-              fv[kl] = ff;
-              ust2[kl] = st;
-            }
-          }
+          const quad::QuadArgs qa{Gr[GN], Gi[GN], ldg, k0, KL, gx[1], ctl.sigma2, alpha};
+          quad::wsr_users(qa, ucache, wcache, lndb[bk], rate, fv, ust2);
+          pc.mark(16);
         } else {
         for (int kl = lane; kl < KL; kl += 32) {
           cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
@@ -1377,6 +1329,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       pc.mark(15);
       if (more && tid == 32) k1_publish();
       cl.sync();
+      xs_fetch();
       pc.mark(5);
       if (a.itU) {  // block iterate of t (solvers.py:487-488), own users / columns
         const size_t it = (size_t)r * a.max_iters + (t - 1);
@@ -1411,9 +1364,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           if (a.latch) ctl.latched = 1;
           if (ctl.switch_it < 0) ctl.switch_it = t;
         }
-        const double wsr = xsum(XS_RATE);
-        const double sv = xsum(XS_FV);
-        int st = xfirst(XS_ST2);
+        const double wsr = xlsum(XS_RATE);
+        const double sv = xlsum(XS_FV);
+        int st = xlfirst(XS_ST2);
         const double total_power = scale == 1.0 ? power : power * scale * scale;
         if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
         double rel = INFINITY;  // solvers.py:474, _rel_change :393-397

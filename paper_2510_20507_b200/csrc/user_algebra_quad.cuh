@@ -42,6 +42,47 @@ __device__ __forceinline__ double lndet_diff4(const double (&pa)[4], const doubl
   return 2.0 * s;
 }
 
+// In-place lower Cholesky (chol_lower) that also returns the inverse pivots:
+// one rsqrt per column instead of sqrt + division, and no divisions in the
+// triangular solves that follow (the per-user algebra is a chain of dependent
+// fp64 operations; a division or square root costs ~20 of them).
+__device__ __forceinline__ bool chol4_inv(cd (&A)[4][4], double (&inv)[4]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double s = A[j][j].r;
+#pragma unroll
+    for (int p = 0; p < j; ++p) s -= cabs2(A[j][p]);
+    ok = ok && (s > 0.0) && isfinite(s);
+    const double r = rsqrt(s);
+    inv[j] = r;
+    A[j][j] = cmk(s * r);
+#pragma unroll
+    for (int i = j + 1; i < 4; ++i) {
+      cd t = A[i][j];
+#pragma unroll
+      for (int p = 0; p < j; ++p) t = csub(t, cmulcb(A[i][p], A[j][p]));
+      A[i][j] = cscale(t, r);
+    }
+  }
+  return ok;
+}
+
+// ln(Π (pa_j ic_j)²): log-det difference from pivots of A and inverse pivots of C
+__device__ __forceinline__ double lndet_diff4i(const double (&pa)[4], const double (&ic)[4]) {
+  double q = 1.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double r = pa[j] * ic[j];
+    q *= r * r;
+  }
+  if (q >= 2.2250738585072014e-308 && q <= 1.7976931348623157e308) return log(q);
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s += log(pa[j]) + log(ic[j]);
+  return 2.0 * s;
+}
+
 // lower triangle of G G^H
 __device__ __forceinline__ void own_gram4(const cd (&G)[4][4], cd (&O)[4][4]) {
 #pragma unroll
@@ -98,13 +139,13 @@ __device__ __forceinline__ void wsr_quad(const cd (&Tg)[4][4], const cd (&G)[4][
     Mx[a][a].r += sigma2;
     Mx[a][a].i = 0.0;
   }
-  const bool ok = chol_lower<4>(Mx);
-  double pa[4], pc[4];
+  double ivp[4];
+  const bool ok = chol4_inv(Mx, ivp);
+  double pa[4], pc[4];  // pivots of A, INVERSE pivots of C
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double pv = Mx[j][j].r;
-    pa[j] = __shfl_sync(0xffffffffu, pv, 0, 4);
-    pc[j] = __shfl_sync(0xffffffffu, pv, 2, 4);
+    pa[j] = __shfl_sync(0xffffffffu, Mx[j][j].r, 0, 4);
+    pc[j] = __shfl_sync(0xffffffffu, ivp[j], 2, 4);
   }
   const unsigned okm = __ballot_sync(0xffffffffu, ok);
   const int lane = threadIdx.x & 31;
@@ -112,7 +153,7 @@ __device__ __forceinline__ void wsr_quad(const cd (&Tg)[4][4], const cd (&G)[4][
   status = 0;
   rate = 0.0;
   if (okq) {
-    const double r = lndet_diff4(pa, pc);
+    const double r = lndet_diff4i(pa, pc);
     rate = ak * (r > 0.0 ? r : 0.0);
   } else {
     status = AMMMSE_STATUS_NONFINITE;
@@ -137,7 +178,8 @@ __device__ __forceinline__ void k1u_quad(const cd (&Tg)[4][4], const cd (&gs)[4]
     L[a][a].r += sigma2;
     L[a][a].i = 0.0;
   }
-  status = chol_lower<4>(L) ? 0 : AMMMSE_STATUS_NONFINITE;
+  double ivp[4];
+  status = chol4_inv(L, ivp) ? 0 : AMMMSE_STATUS_NONFINITE;
 #pragma unroll
   for (int a = 0; a < 4; ++a) piv[a] = L[a][a].r;
 #pragma unroll
@@ -145,14 +187,14 @@ __device__ __forceinline__ void k1u_quad(const cd (&Tg)[4][4], const cd (&gs)[4]
     cd t = gs[i];
 #pragma unroll
     for (int p = 0; p < i; ++p) t = csub(t, cmul(L[i][p], u[p]));
-    u[i] = cscale(t, 1.0 / L[i][i].r);
+    u[i] = cscale(t, ivp[i]);
   }
 #pragma unroll
   for (int i = 3; i >= 0; --i) {  // backward: L^H x = y
     cd t = u[i];
 #pragma unroll
     for (int p = i + 1; p < 4; ++p) t = csub(t, cmulc(L[p][i], u[p]));
-    u[i] = cscale(t, 1.0 / L[i][i].r);
+    u[i] = cscale(t, ivp[i]);
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) ucol[a * 4 + s] = u[a];
@@ -177,7 +219,7 @@ __device__ __forceinline__ void k1u_quad(const cd (&Tg)[4][4], const cd (&gs)[4]
 
 // Weight half of K1 (k1_part_w), lane s = column s: C = Tg + σ² I − G G^H = Lc Lc^H,
 // Y = Lc^{-1} G, W = I + Y^H Y.  Writes column s of W to wcol[p * 4 + s]; returns
-// the pivots of C and the positive-definiteness flag.  `yscr`: 16 cd of scratch.
+// the INVERSE pivots of C and the positive-definiteness flag.  `yscr`: 16 cd of scratch.
 __device__ __forceinline__ void k1w_quad(const cd (&Tg)[4][4], const cd (&G)[4][4], const cd (&gs)[4],
                                          double sigma2, int s, cd* yscr, cd* wcol, double (&piv)[4], int& pd) {
   cd O[4][4], L[4][4];
@@ -191,16 +233,14 @@ __device__ __forceinline__ void k1w_quad(const cd (&Tg)[4][4], const cd (&G)[4][
     L[a][a].r += sigma2;
     L[a][a].i = 0.0;
   }
-  pd = chol_lower<4>(L) ? 1 : 0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) piv[a] = L[a][a].r;
+  pd = chol4_inv(L, piv) ? 1 : 0;  // piv: INVERSE pivots of C
   cd y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     cd t = gs[i];
 #pragma unroll
     for (int p = 0; p < i; ++p) t = csub(t, cmul(L[i][p], y[p]));
-    y[i] = cscale(t, 1.0 / L[i][i].r);
+    y[i] = cscale(t, piv[i]);
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) yscr[a * 4 + s] = y[a];
@@ -237,7 +277,7 @@ __device__ __forceinline__ void k1c_quad(const cd (&Ufull)[4][4], const cd (&us)
     const double cond = sqrt(nT) * sqrt(nW);  // ‖T‖_F ‖W‖_F >= cond_2(T)
     if ((!pdc || !isfinite(cond) || cond > kCondLimitUA) && status == 0)
       status = AMMMSE_STATUS_ILL_CONDITIONED;
-    if (pdc && status != AMMMSE_STATUS_NONFINITE) lndetw = lndet_diff4(piva, pivc);
+    if (pdc && status != AMMMSE_STATUS_NONFINITE) lndetw = lndet_diff4i(piva, pivc);  // pivc: inverse pivots
   } else {
     trw = s == 0 ? tcol[0].r : (s == 1 ? tcol[1].r : (s == 2 ? tcol[2].r : tcol[3].r));  // W = I
   }
@@ -261,6 +301,178 @@ __device__ __forceinline__ void k1c_quad(const cd (&Ufull)[4][4], const cd (&us)
 #pragma unroll
     for (int p = 0; p < 4; ++p) cfma(acc, pscr[a * 4 + p], tcol[p]);
     dcol[a] = cmk(-acc.r, -acc.i);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-level drivers.  NOT inlined on purpose: inside the persistent solver
+// kernel the register allocator is saturated (255 registers, spills around
+// every fp64 chain, and every cluster barrier flushes L1, where the spills
+// live); as separate functions they get their own allocation.  All operands
+// are shared-memory pointers.
+//   G planes: fp32, row stride ldg, the CTA's own columns; user kl (global
+//   k0 + kl) has its N x d diagonal block at rows 4 (k0 + kl), columns 4 kl.
+//   gram: reduced Grams, 16 cd per GLOBAL user.  ucache / wcache: 16 cd per own user.
+// ---------------------------------------------------------------------------
+struct QuadArgs {
+  const float* Gr;
+  const float* Gi;
+  int ldg, k0, KL;
+  const cd* gram;
+  double sigma2;
+  const double* alpha;
+};
+
+// WSR(t): rate[kl], fv[kl], ust2[kl] of the own users (one full warp)
+static __device__ __noinline__ void wsr_users(QuadArgs q, const cd* ucache, const cd* wcache, const double* lndetw,
+                                       double* rate, double* fv, double* ust2) {
+  __builtin_assume(__isShared(q.Gr));
+  __builtin_assume(__isShared(q.Gi));
+  __builtin_assume(__isShared(q.gram));
+  __builtin_assume(__isShared(q.alpha));
+  __builtin_assume(__isShared(ucache));
+  __builtin_assume(__isShared(wcache));
+  __builtin_assume(__isShared(lndetw));
+  __builtin_assume(__isShared(rate));
+  const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
+  for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
+    const bool act = kl0 + ul < q.KL;
+    const int kl = act ? kl0 + ul : 0;
+    cd Tg[4][4], G[4][4], U[4][4], gs[4], us[4], ws[4];
+    const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
+    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        Tg[p][c] = g[p * 4 + c];
+        G[p][c] = cmk((double)q.Gr[gbase + p * q.ldg + c], (double)q.Gi[gbase + p * q.ldg + c]);
+        U[p][c] = ucache[kl * 16 + p * 4 + c];
+      }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {  // column sc (no dynamic register indexing)
+      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+      us[p] = ucache[kl * 16 + p * 4 + sc];
+      ws[p] = wcache[kl * 16 + p * 4 + sc];
+    }
+    const double wss = wcache[kl * 16 + sc * 4 + sc].r;
+    double rr, ff;
+    int st;
+    wsr_quad(Tg, G, gs, q.sigma2, q.alpha[kl], U, us, ws, wss, lndetw[kl], sc, rr, ff, st);
+    if (act && sc == 0) {
+      rate[kl] = rr;
+      fv[kl] = ff;
+      ust2[kl] = st;
+    }
+  }
+}
+
+struct K1Out4 {  // destinations of K1 (own users unless noted)
+  cd* ucache;        // 16 cd per user
+  cd* wcache;        // 16 cd per user
+  double* lndetw;
+  double* fu;
+  double* fw;
+  double* ust;
+  float2* Uall;      // fp32, 16 per GLOBAL user
+  float2* Pall;      // fp32, 16 per GLOBAL user
+  float2* Down;      // fp32, 16 per own user
+  double* scratch;   // kScratch doubles per own user
+};
+
+// K1(t+1), weight half (warp 2 of the block; pairs with k1_recv_users through
+// named barrier 1, 64 threads, once per pass of 8 users)
+static __device__ __noinline__ void k1_weight_users(QuadArgs q, K1Out4 o) {
+  const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
+  for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
+    const bool act = kl0 + ul < q.KL;
+    const int kl = act ? kl0 + ul : 0;
+    cd Tg[4][4], G[4][4], gs[4];
+    const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
+    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        Tg[p][c] = g[p * 4 + c];
+        G[p][c] = cmk((double)q.Gr[gbase + p * q.ldg + c], (double)q.Gi[gbase + p * q.ldg + c]);
+      }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+    double* scr = o.scratch + (size_t)kl * kScratch;
+    double pivc[4];
+    int pd;
+    k1w_quad(Tg, G, gs, q.sigma2, sc, reinterpret_cast<cd*>(scr), o.wcache + (size_t)kl * 16, pivc, pd);
+    if (sc == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) scr[64 + j] = pivc[j];
+      scr[68] = (double)pd;
+    }
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+  }
+}
+
+// K1(t+1), receiver half + combine (warp 1).  wprev / lndet_wprev: the previous
+// iteration's W bank (f_after_u, solvers.py:447).
+static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd* wprev, const double* lndet_wprev,
+                                           bool weighted) {
+  const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
+  for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
+    const bool act = kl0 + ul < q.KL;
+    const int kl = act ? kl0 + ul : 0;
+    cd Tg[4][4], gs[4], Wprow[4];
+    const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
+    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+#pragma unroll
+      for (int c = 0; c <= p; ++c) Tg[p][c] = g[p * 4 + c];
+      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+      Wprow[p] = wprev[kl * 16 + sc * 4 + p];
+    }
+    double* scr = o.scratch + (size_t)kl * kScratch;
+    cd* ucol = o.ucache + (size_t)kl * 16;
+    cd* wcol = o.wcache + (size_t)kl * 16;
+    cd Ufull[4][4], us[4], tcol[4];
+    double fu_, nT, piva[4];
+    int st;
+    k1u_quad(Tg, gs, q.sigma2, q.alpha[kl], Wprow, lndet_wprev[kl], sc, ucol, Ufull, us, tcol, fu_, nT, piva, st);
+    cd wcs[4];
+    double pivc[4] = {1.0, 1.0, 1.0, 1.0};
+    int pdc = 1;
+    if (weighted) {
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        wcs[p] = wcol[p * 4 + sc];
+        pivc[p] = scr[64 + p];
+      }
+      pdc = (int)scr[68];
+    } else {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) wcs[p] = cmk(p == sc ? 1.0 : 0.0);
+    }
+    cd pcol[4], dcol[4];
+    double fw_, lnw;
+    k1c_quad(Ufull, us, tcol, nT, piva, wcs, pivc, pdc, q.alpha[kl], weighted, sc,
+             reinterpret_cast<cd*>(scr + 32), pcol, dcol, fw_, lnw, st);
+    if (act) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {  // row p, column sc
+        const int ig = ((q.k0 + kl) * 4 + p) * 4 + sc, il = (kl * 4 + p) * 4 + sc;
+        o.Uall[ig] = make_float2((float)us[p].r, (float)us[p].i);
+        o.Pall[ig] = make_float2((float)pcol[p].r, (float)pcol[p].i);
+        o.Down[il] = make_float2((float)dcol[p].r, (float)dcol[p].i);
+        if (!weighted) wcol[p * 4 + sc] = wcs[p];
+      }
+      if (sc == 0) {
+        o.lndetw[kl] = lnw;
+        o.fu[kl] = fu_;
+        o.fw[kl] = fw_;
+        o.ust[kl] = st;
+      }
+    }
   }
 }
 
