@@ -475,7 +475,8 @@ def main():
     peak = peak32 if w.dtype == np.complex64 else peak64
     sm_mhz = (clk.get("sm_max_mhz") or 1965.0)
     nominal = 148 * 128 * 2 * sm_mhz * 1e6 if w.dtype == np.complex64 else 148 * 64 * 2 * sm_mhz * 1e6
-    kname = ("ammmse_cluster_kernel" if engine_plan["cluster"] else "ammmse_solve_kernel")
+    kname = ("ammmse_tc2_kernel" if engine_plan["tensor_cores"] == 2 else
+             "ammmse_cluster_kernel" if engine_plan["cluster"] else "ammmse_solve_kernel")
     kname += (f"<C={engine_plan['cluster']}>" if engine_plan["cluster"] else "")
     if engine_plan["tensor_cores"]:
         # tcgen05 3xTF32 GEMMs: the bound is the tensor pipe; its fp32-equivalent

@@ -79,7 +79,7 @@ int pick_threads(const AmmmseDims* d);
 
 int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_cores, Plan* p) {
   const ammmse::KernelEntry* e = lookup(d);
-  if (!e) return AMMMSE_ERR_UNSUPPORTED;
+  if (!e || !e->smem_bytes || !e->cluster_smem_bytes) return AMMMSE_ERR_UNSUPPORTED;  // (empty: dev builds)
   int lim = max_smem_optin();
   if (lim <= 0) lim = 232448;  // sm_100 opt-in limit (no device to query)
   p->e = e;
@@ -417,6 +417,12 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
   a.scratch = reinterpret_cast<unsigned char*>(workspace) + 256;
   a.tcm = plan.cluster ? plan.tc : 0;
   a.tc_stages = plan.stages;
+  {  // tuning knob (A/B measurements): AMMMSE_TC2_DEFER=1 moves WSR(t) into GEMM-A(t+1)
+     // once the stage is latched.  Off by default: measured 1872 vs 1980 realizations/s on
+     // BASELINE large (K1(t+1) is as long as WSR(t), so hiding WSR alone does not pay).
+    const char* de = getenv("AMMMSE_TC2_DEFER");
+    a.tc_defer = (de && de[0] == '1') ? 1 : 0;
+  }
   if (a.tcm) {  // H planes after the V_old slots, 256-byte aligned
     int sms2 = 0;
     cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev);

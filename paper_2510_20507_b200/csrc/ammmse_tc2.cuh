@@ -74,7 +74,7 @@ struct T2Layout {
   int acc_cols;  // TMEM columns of the accumulators; the precoders, then G_old follow
   int v_cols;
   size_t nG;     // floats per G plane
-  size_t oRing, oB, oG0, oG1, oU, oP, oD, dbl_off, bytes;  // byte offsets
+  size_t oRing, oB, oG0, oG1, oU, oP, oD, oGk, dbl_off, bytes;  // byte offsets
 
   __host__ __device__ void init(int M_, int K_, int C_, int S_) {
     M = M_;
@@ -103,7 +103,8 @@ struct T2Layout {
     oU = (oG1 + 2 * nG * 4 + 15) & ~(size_t)15;  // RC<float>[K*NN*DD]
     oP = oU + (size_t)K * NN * DD * 8;
     oD = oP + (size_t)K * NN * DD * 8;           // RC<float>[KL*NN*DD]
-    dbl_off = (oD + (size_t)KL * NN * DD * 8 + 15) & ~(size_t)15;
+    oGk = oD + (size_t)KL * NN * DD * 8;         // float[2][KL*NN*DD]: saved diagonal blocks of G_new
+    dbl_off = (oGk + (size_t)KL * NN * DD * 8 + 15) & ~(size_t)15;
     bytes = dbl_off + dbl_count() * sizeof(double);
   }
   // fp64 region: as CLayout (gx[2], ucache[2], wcache[2], lndetw[2], 7 per-user
@@ -270,9 +271,14 @@ constexpr int kProducerWarp = 1, kProducerWarp2 = 3;
 // 237 cycles, a 16 KB bulk copy 520-700 cycles of latency (83 B/clk back to
 // back): a stage turns around in ~1.1 k cycles, which a 3-stage ring cannot hide
 // behind ~300 cycles of MMAs per chunk — hence the 7 stages.
-template <class Clock>
+struct NoSide {
+  __device__ __forceinline__ void operator()() const {}
+};
+constexpr int kSideWarp = 4;  // runs `side` during the MMA loop (a warp with no pipeline role)
+
+template <class Clock, class Side = NoSide>
 __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict__ Ag, int nch, int ncol,
-                                     int nsets, const float* __restrict__ next_Ag) {
+                                     int nsets, const float* __restrict__ next_Ag, Side side = Side()) {
   constexpr uint32_t a_bytes = 4u * 128u * KW * 4u;  // one chunk: 4 planes x 128 rows x KW floats
   constexpr uint32_t a_plane = 128u * KW * 4u;
   const uint32_t have = p.have;
@@ -391,6 +397,8 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
     if (warp == kMmaWarp) umma::mbar_wait_spin(p.fin, p.call & 1u);  // all MMAs of this call completed
     pc.mark2(18);  // tail: the last MMAs
     p.cm = cm;
+  } else if (warp == kSideWarp) {
+    side();
   }
   p.have = npf;
   p.call += 1;
@@ -482,6 +490,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
   RC<R>* Pall = reinterpret_cast<RC<R>*>(smem + L.oP);
   RC<R>* Down = reinterpret_cast<RC<R>*>(smem + L.oD);
   unsigned char* bfull = smem + L.oB;
+  float* gkk_save = reinterpret_cast<float*>(smem + L.oGk);
   double* dp = reinterpret_cast<double*>(smem + L.dbl_off);
   cd* gx[2];
   gx[0] = reinterpret_cast<cd*>(dp); dp += 2 * K * NN * NN;
@@ -767,7 +776,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       // four lanes per user (user_algebra_quad.cuh)
       if (warp != 1 && warp != 2) return;
       if (warp == 2 && !weighted) return;
-      const quad::QuadArgs qa{Gr[gsrc], Gi[gsrc], ldg, k0, KL, gx[0], ctl.sigma2, alpha};
+      const quad::QuadArgs qa{Gr[gsrc] + (size_t)k0 * NN * ldg, Gi[gsrc] + (size_t)k0 * NN * ldg,
+                              NN * ldg + DD, ldg, k0, KL, gx[0], ctl.sigma2, alpha, a.trace != nullptr};
       const quad::K1Out4 ko{ucb[bout], wcb[bout], lndb[bout], fu, fw, ust,
                             reinterpret_cast<float2*>(Uall), reinterpret_cast<float2*>(Pall),
                             reinterpret_cast<float2*>(Down), k1w};
@@ -1216,6 +1226,119 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     pc.mark(9);
 
     // ---------------- main loop (solvers.py:440-505), software-pipelined ----------------
+    // State machine of iteration te (solvers.py:449-505) on thread 0, from the
+    // local exchange copies; identical decisions in every CTA.
+    auto state_machine = [&](int te, bool wn_e, double power, double scale) {
+      if (!ctl.latched && wn_e) {
+        if (a.latch) ctl.latched = 1;
+        if (ctl.switch_it < 0) ctl.switch_it = te;
+      }
+      const double wsr = xlsum(XS_RATE);
+      const double sv = xlsum(XS_FV);
+      int st = xlfirst(XS_ST2);
+      const double total_power = scale == 1.0 ? power : power * scale * scale;
+      if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
+      double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
+      if (te > 1) {
+        const double den = fabs(ctl.wsr_last);
+        rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
+      }
+      ctl.wsr_prev = ctl.wsr_last;
+      ctl.wsr_last = wsr;
+      ctl.nhist += 1;
+      ctl.iters = te;
+      ctl.wsr = wsr;
+      ctl.f_v = sv;
+      ctl.weighted_now = wn_e;
+      ctl.last_weighted = wn_e;
+      if (a.trace && crank == 0) {
+        double* tr = a.trace + ((size_t)r * a.max_iters + (te - 1)) * kTraceFields;
+        tr[AMMMSE_TRACE_T] = (double)te;
+        tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
+        tr[AMMMSE_TRACE_F_VALUE] = sv;
+        tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
+        tr[AMMMSE_TRACE_STAGE] = wn_e ? 1.0 : 0.0;
+        tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
+        tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
+        tr[AMMMSE_TRACE_F_AFTER_V] = sv;
+        tr[AMMMSE_TRACE_REL_CHANGE] = rel;
+      }
+      ctl.running_max = fmax(ctl.running_max, wsr);  // divergence detector (solvers.py:490-500)
+      if (wsr < 0.5 * ctl.running_max)
+        ctl.drop_streak += 1;
+      else
+        ctl.drop_streak = 0;
+      if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
+      if (st) {
+        ctl.status = st;
+        ctl.stop = 1;
+      } else if (wn_e && rel <= a.eps2) {  // stop test (:503-505)
+        ctl.converged = 1;
+        ctl.stop = 1;
+      }
+      ctl.wn_next = stage_flag();
+    };
+    // WSR of the own users from the reduced Gram gx[1] and the diagonal blocks
+    // at (gr, gi): per-user rates / f_after_v, then the CTA partials -> exchange
+    // slots.  One full warp.
+    auto wsr_warp = [&](const R* gr, const R* gi, int ustride, int rstride, int bank) {
+      const cd* ucache = ucb[bank];
+      const cd* wcache = wcb[bank];
+      if constexpr (NN == 4 && DD == 4) {  // four lanes per user (user_algebra_quad.cuh)
+        const quad::QuadArgs qa{gr, gi, ustride, rstride, k0, KL, gx[1], ctl.sigma2, alpha, a.trace != nullptr};
+        quad::wsr_users(qa, ucache, wcache, lndb[bank], rate, fv, ust2);
+      } else {
+        for (int kl = lane; kl < KL; kl += 32) {
+          cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
+          gram_of(1, kl, Tg);
+#pragma unroll
+          for (int p = 0; p < NN; ++p)
+#pragma unroll
+            for (int q = 0; q < DD; ++q) {
+              const int idx = kl * ustride + p * rstride + q;
+              Gkk[p][q] = cmk((double)gr[idx], (double)gi[idx]);
+              U[p][q] = ucache[(kl * NN + p) * DD + q];
+            }
+#pragma unroll
+          for (int p = 0; p < DD; ++p)
+#pragma unroll
+            for (int q = 0; q < DD; ++q) W[p][q] = wcache[(kl * DD + p) * DD + q];
+          double rr, ff;
+          int st;
+          wsr_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], U, W, lndb[bank][kl], rr, ff, st);
+          rate[kl] = rr;
+          fv[kl] = ff;
+          ust2[kl] = st;
+        }
+      }
+      __syncwarp();
+      double sr = 0.0, sv = 0.0;
+      int f2 = KL;
+      for (int kl = lane; kl < KL; kl += 32) {
+        sr += rate[kl];
+        sv += fv[kl];
+        if (f2 == KL && ust2[kl] != 0.0) f2 = kl;
+      }
+      sr = warp_allsum(sr);
+      sv = warp_allsum(sv);
+      f2 = __reduce_min_sync(0xffffffffu, f2);
+      if (lane == 0) {
+        xs[XS_RATE] = sr;
+        xs[XS_FV] = sv;
+        xs[XS_ST2] = f2 < KL ? ust2[f2] : 0.0;
+      }
+    };
+    // Deferred mode: once the weighted stage is latched the stage flag cannot
+    // change any more, so iteration t+1 may start before WSR(t) is known: WSR(t)
+    // then runs on a spare warp DURING GEMM-A(t+1), its cluster exchange rides on
+    // the ‖X‖² barrier and the state machine of t runs after GEMM-B(t+1)'s MMAs.
+    // A stop discovered there discards the speculative step: V(t) is still X[xc]
+    // (the step wrote the other TMEM buffer); G is rebuilt for the exit pass.
+    // Not used with traces / recorded iterates (their rows are written in order).
+    const bool can_defer = a.tc_defer && a.latch && !a.trace && !a.itU;
+    bool pending = false;   // WSR(t-1) / state machine of t-1 outstanding
+    bool need_g = false;    // exit: G buffers do not hold G(V_final)
+    double power_p = 0.0, scale_p = 1.0;  // ‖X‖², scale of the pending iteration
     for (int t = 1; t <= a.max_iters; ++t) {
       const int bk = t & 1;  // bank holding K1(t)'s U / W / ln det W
       if (tid == 0) {        // K1(t) results (published before the last cluster barrier)
@@ -1234,12 +1357,19 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
       __syncthreads();
       pc.mark(0);
-      if (ctl.stop) break;
+      if (ctl.stop && !pending) break;
+      // (pending: the K1(t) failure belongs to a step that may still be discarded;
+      // it is acted on after the state machine of t-1 below)
       build_yhat(GE);
       __syncthreads();
       pc.mark(1);
-      // ∇ = H^H Ŷ
-      tc2::gemm(pipe, pc, hpA, nchA, ncol, nsets, hpB);
+      // ∇ = H^H Ŷ  (deferred mode: WSR(t-1) on the side warp meanwhile)
+      if (pending) {
+        tc2::gemm(pipe, pc, hpA, nchA, ncol, nsets, hpB,
+                  [&]() { wsr_warp(gkk_save, gkk_save + KL * NN * DD, NN * DD, DD, (t - 1) & 1); });
+      } else {
+        tc2::gemm(pipe, pc, hpA, nchA, ncol, nsets, hpB);
+      }
       pc.mark(10);
       const int xo = 1 - xc;
       double pw = epilogue_a(xc, xo, vsc(xc), vsc(xo), (float)ctl.step, (float)ctl.omega, extrap, true);
@@ -1251,7 +1381,27 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       // G' = H X_new while the cluster sums ‖X_new‖² (the projection scale is lazy)
       tc2::gemm(pipe, pc, hpB, nchB, ncol, nsets, hpA);
       asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      const double power = xsum_block(XS_POWER);
+      xs_fetch();
+      if (tid == 0) {
+        const int k1_stop = ctl.stop, k1_status = ctl.status;  // K1(t) failure noted above
+        if (pending) {
+          ctl.stop = 0;
+          ctl.status = 0;
+          state_machine(t - 1, true, power_p, scale_p);
+          if (!ctl.stop && k1_stop) {  // iteration t itself failed in K1(t)
+            ctl.status = k1_status;
+            ctl.stop = 2;  // (2: stop without discarding... K1(t) failed: nothing of t is kept)
+          }
+        }
+        s_power = xlsum(XS_POWER);
+      }
+      __syncthreads();
+      if (pending && ctl.stop) {  // discard the speculative step
+        need_g = true;
+        break;
+      }
+      pending = false;
+      const double power = s_power;
       double scale = 1.0;
       if (!(power <= ctl.pmax)) scale = sqrt(ctl.pmax / power);  // project_sum_power :257-263
       if (xo) vs1 = (float)scale; else vs0 = (float)scale;
@@ -1267,6 +1417,15 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       else if (more)
         gram_quad(Gr[GE], Gi[GE], gx[0], tid - 128, 128);
       const bool wn_spec = ctl.latched || wn;
+      const bool defer = can_defer && more && ctl.latched;  // WSR(t) during GEMM-A(t+1)
+      if (defer) {  // the ring will overwrite N: keep the own users' diagonal blocks
+        for (int i = tid; i < KL * NN * DD; i += blockDim.x) {
+          const int kl = i / (NN * DD), rem = i - kl * NN * DD, p = rem / DD, q = rem - p * DD;
+          const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + q;
+          gkk_save[i] = Gr[GN][idx];
+          gkk_save[KL * NN * DD + i] = Gi[GN][idx];
+        }
+      }
       pc.mark(12);
       cl.sync();
       pc.mark(13);
@@ -1274,55 +1433,18 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       if (more) gram_reduce(0);
       __syncthreads();
       pc.mark(4);
-      if (tid < 32) {  // warp 0: rates / f_after_v of own users, CTA partials
-        const cd* ucache = ucb[bk];
-        const cd* wcache = wcb[bk];
-        if constexpr (NN == 4 && DD == 4) {  // four lanes per user (user_algebra_quad.cuh)
-          const quad::QuadArgs qa{Gr[GN], Gi[GN], ldg, k0, KL, gx[1], ctl.sigma2, alpha};
-          quad::wsr_users(qa, ucache, wcache, lndb[bk], rate, fv, ust2);
-          pc.mark(16);
-        } else {
-        for (int kl = lane; kl < KL; kl += 32) {
-          cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
-          gram_of(1, kl, Tg);
-#pragma unroll
-          for (int p = 0; p < NN; ++p)
-#pragma unroll
-            for (int s = 0; s < DD; ++s) {
-              const int idx = ((k0 + kl) * NN + p) * ldg + kl * DD + s;
-              Gkk[p][s] = cmk((double)Gr[GN][idx], (double)Gi[GN][idx]);
-              U[p][s] = ucache[(kl * NN + p) * DD + s];
-            }
-#pragma unroll
-          for (int p = 0; p < DD; ++p)
-#pragma unroll
-            for (int q = 0; q < DD; ++q) W[p][q] = wcache[(kl * DD + p) * DD + q];
-          double rr, ff;
-          int st;
-          wsr_math<NN, DD>(Tg, Gkk, ctl.sigma2, alpha[kl], U, W, lndb[bk][kl], rr, ff, st);
-          rate[kl] = rr;
-          fv[kl] = ff;
-          ust2[kl] = st;
-        }
-        }
-        __syncwarp();
-        double sr = 0.0, sv = 0.0;
-        int f2 = KL;
-        for (int kl = lane; kl < KL; kl += 32) {
-          sr += rate[kl];
-          sv += fv[kl];
-          if (f2 == KL && ust2[kl] != 0.0) f2 = kl;
-        }
-        sr = warp_allsum(sr);
-        sv = warp_allsum(sv);
-        f2 = __reduce_min_sync(0xffffffffu, f2);
-        if (lane == 0) {
-          xs[XS_RATE] = sr;
-          xs[XS_FV] = sv;
-          xs[XS_ST2] = f2 < KL ? ust2[f2] : 0.0;
-        }
+      if (tid < 32) {  // warp 0: WSR(t) unless deferred
+        if (!defer)
+          wsr_warp(Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg, NN * ldg + DD, ldg, bk);
       } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
+#if AMMMSE_PHASES
+        const long long tk0 = clock64();
+#endif
         k1_pipelined(GE, wn_spec, bk, bk ^ 1);
+#if AMMMSE_PHASES
+        if (a.prof && (tid == 32 || tid == 64) && blockIdx.x == 0)
+          atomicAdd(a.prof + (tid == 32 ? 17 : 18), (unsigned long long)(clock64() - tk0));
+#endif
       }
       pc.mark(14);
       __syncthreads();
@@ -1359,61 +1481,17 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           }
         umma::fence_before();
       }
-      if (tid == 0) {  // state machine of iteration t, identical in every CTA
-        if (!ctl.latched && wn) {
-          if (a.latch) ctl.latched = 1;
-          if (ctl.switch_it < 0) ctl.switch_it = t;
-        }
-        const double wsr = xlsum(XS_RATE);
-        const double sv = xlsum(XS_FV);
-        int st = xlfirst(XS_ST2);
-        const double total_power = scale == 1.0 ? power : power * scale * scale;
-        if (!isfinite(wsr) || !isfinite(power)) st = AMMMSE_STATUS_NONFINITE;
-        double rel = INFINITY;  // solvers.py:474, _rel_change :393-397
-        if (t > 1) {
-          const double den = fabs(ctl.wsr_last);
-          rel = den == 0.0 ? INFINITY : fabs(wsr - ctl.wsr_last) / den;
-        }
-        ctl.wsr_prev = ctl.wsr_last;
-        ctl.wsr_last = wsr;
-        ctl.nhist += 1;
-        ctl.iters = t;
-        ctl.wsr = wsr;
-        ctl.f_v = sv;
-        ctl.weighted_now = wn;
-        ctl.last_weighted = wn;
-        if (a.trace && crank == 0) {
-          double* tr = a.trace + ((size_t)r * a.max_iters + (t - 1)) * kTraceFields;
-          tr[AMMMSE_TRACE_T] = (double)t;
-          tr[AMMMSE_TRACE_WSR_BITS] = wsr / kLn2;
-          tr[AMMMSE_TRACE_F_VALUE] = sv;
-          tr[AMMMSE_TRACE_TOTAL_POWER] = total_power;
-          tr[AMMMSE_TRACE_STAGE] = wn ? 1.0 : 0.0;
-          tr[AMMMSE_TRACE_F_AFTER_U] = ctl.f_u;
-          tr[AMMMSE_TRACE_F_AFTER_W] = ctl.f_w;
-          tr[AMMMSE_TRACE_F_AFTER_V] = sv;
-          tr[AMMMSE_TRACE_REL_CHANGE] = rel;
-        }
-        ctl.running_max = fmax(ctl.running_max, wsr);  // divergence detector (solvers.py:490-500)
-        if (wsr < 0.5 * ctl.running_max)
-          ctl.drop_streak += 1;
-        else
-          ctl.drop_streak = 0;
-        if (ctl.drop_streak >= 5 && st == 0) st = AMMMSE_STATUS_UNSTABLE;
-        if (st) {
-          ctl.status = st;
-          ctl.stop = 1;
-        } else {
-          if (wn && rel <= a.eps2) {  // stop test (:503-505)
-            ctl.converged = 1;
-            ctl.stop = 1;
-          }
-        }
-        ctl.wn_next = stage_flag();
+      if (defer) {  // state machine of t postponed; the stage flag stays latched
+        pending = true;
+        power_p = power;
+        scale_p = scale;
+        if (tid == 0) ctl.wn_next = 1;
+      } else if (tid == 0) {
+        state_machine(t, wn, power, scale);
       }
       __syncthreads();
       pc.mark(6);
-      if (ctl.stop) break;
+      if (!defer && ctl.stop) break;
       wn = ctl.wn_next != 0;
       if (more && wn != wn_spec) {  // mis-speculated stage flag: redo K1(t+1) (same inputs)
         k1_phase(GE, wn, true, bk, bk ^ 1);
@@ -1427,6 +1505,27 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     // ---------------- exit: stationarity residual (solvers.py:400-412) ----------------
     double residual = NAN;
     if (ctl.status == 0) {
+      if (need_g) {  // a speculative step was discarded: rebuild G = H V_final into N
+        tc2::drain(pipe);  // (chunks prefetched for the GEMM-A that will not run)
+        __syncthreads();
+        for (int t = 0; t < nmtA; ++t)
+          for (int q0 = 16 * cgrp; q0 < ncol; q0 += 32) {
+            float xr[16], xi[16];
+            load_x(xc, t, q0, xr, xi);
+            const int row = 128 * t + row_in_tile;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              b_store(q0 + j, row, xr[j] * vsc(xc));
+              b_store(ncol + q0 + j, row, xi[j] * vsc(xc));
+            }
+          }
+        umma::fence_proxy_async();
+        umma::fence_before();
+        __syncthreads();
+        tc2::gemm(pipe, pc, hpB, nchB, ncol, nsets, hpA);
+        epilogue_b(1.f, 0.f, false);
+        __syncthreads();
+      }
       const bool weighted = ctl.latched || ctl.last_weighted;
       for (int i = tid; i < KN * ldg; i += blockDim.x) {  // fresh U / W on the final G (scratch: E)
         Gr[GE][i] = Gr[GN][i];

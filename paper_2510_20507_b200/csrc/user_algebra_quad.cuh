@@ -19,7 +19,8 @@
 namespace ammmse {
 namespace quad {
 
-constexpr int kScratch = 72;  // doubles per user: Y, P (16 cd each), pivots of C, flag
+// doubles per user: Y [0,32), P [32,64), T [64,96) (16 cd each), then ‖T‖², pivots of A, status
+constexpr int kScratch = 104;
 
 __device__ __forceinline__ double qsum(double v) {
   v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -104,8 +105,10 @@ __device__ __forceinline__ void own_gram4(const cd (&G)[4][4], cd (&O)[4][4]) {
 // push it to local memory.
 __device__ __forceinline__ void wsr_quad(const cd (&Tg)[4][4], const cd (&G)[4][4], const cd (&gs)[4],
                                          double sigma2, double ak, const cd (&U)[4][4], const cd (&us)[4],
-                                         const cd (&ws)[4], double wss, double lndetw, int s, double& rate,
-                                         double& fv, int& status) {
+                                         const cd (&ws)[4], double wss, double lndetw, int s, bool want_f,
+                                         double& rate, double& fv, int& status) {
+  fv = 0.0;
+  if (want_f) {  // f_after_v feeds the trace only
   // column s of A U and of U W
   cd au[4], uw[4];
 #pragma unroll
@@ -126,6 +129,7 @@ __device__ __forceinline__ void wsr_quad(const cd (&Tg)[4][4], const cd (&G)[4][
     term += uw[a].r * z.r + uw[a].i * z.i;  // Re(conj(uw) z)
   }
   fv = ak * (qsum(term) - lndetw);
+  }
   // lanes 0, 1 factor A = Tg + σ² I, lanes 2, 3 factor C = A − G G^H
   cd O[4][4], Mx[4][4];
   own_gram4(G, O);
@@ -165,7 +169,7 @@ __device__ __forceinline__ void wsr_quad(const cd (&Tg)[4][4], const cd (&G)[4][
 // (‖T‖_F², quad sum), piv (Cholesky pivots of A), status.  `Ufull` returns the
 // whole U (read back from `ucol` after a warp barrier).
 __device__ __forceinline__ void k1u_quad(const cd (&Tg)[4][4], const cd (&gs)[4], double sigma2, double ak,
-                                         const cd (&Wprow)[4], double lndet_wprev, int s, cd* ucol,
+                                         const cd (&Wprow)[4], double lndet_wprev, int s, bool want_f, cd* ucol,
                                          cd (&Ufull)[4][4], cd (&u)[4], cd (&tcol)[4], double& fu, double& nT,
                                          double (&piv)[4], int& status) {
   cd L[4][4];
@@ -214,7 +218,7 @@ __device__ __forceinline__ void k1u_quad(const cd (&Tg)[4][4], const cd (&gs)[4]
     tr += Wprow[p].r * tcol[p].r - Wprow[p].i * tcol[p].i;  // Re(Wprev[s][p] T[p][s])
   }
   nT = qsum(nt);
-  fu = ak * (qsum(tr) - lndet_wprev);
+  fu = want_f ? ak * (qsum(tr) - lndet_wprev) : 0.0;
 }
 
 // Weight half of K1 (k1_part_w), lane s = column s: C = Tg + σ² I − G G^H = Lc Lc^H,
@@ -255,13 +259,14 @@ __device__ __forceinline__ void k1w_quad(const cd (&Tg)[4][4], const cd (&G)[4][
   }
 }
 
-// K1 combine (k1_combine), lane s = column s, after the W columns are visible.
-//   wcol_s[p] = W[p][s];  Ufull, tcol, nT, piva from k1u_quad;  pivc, pdc from k1w_quad.
-// Outputs column s of P = α U W and D = −P T, fw, lndetw, and the updated status.
-__device__ __forceinline__ void k1c_quad(const cd (&Ufull)[4][4], const cd (&us)[4], const cd (&tcol)[4], double nT,
-                                         const double (&piva)[4], const cd (&wcol_s)[4],
-                                         const double (&pivc)[4], int pdc, double ak, bool weighted, int s,
-                                         cd* pscr, cd (&pcol)[4], cd (&dcol)[4], double& fw, double& lndetw,
+// K1 combine (k1_combine), statistics half, lane s = column s: the ill-conditioning
+// test on ‖T‖_F ‖W‖_F, ln det W = ln det A − ln det C and f_after_w.
+//   wcol_s[p] = W[p][s], tcol[p] = T[p][s], nT = ‖T‖_F²; piva: pivots of A; ipivc:
+//   INVERSE pivots of C.  want_f = false skips the log and the trace (they feed
+//   the recorded trace only).
+__device__ __forceinline__ void k1c_stat(const cd (&tcol)[4], double nT, const double (&piva)[4],
+                                         const cd (&wcol_s)[4], const double (&ipivc)[4], int pdc, double ak,
+                                         bool weighted, bool want_f, int s, double& fw, double& lndetw,
                                          int& status) {
   lndetw = 0.0;
   double trw = 0.0;
@@ -274,14 +279,21 @@ __device__ __forceinline__ void k1c_quad(const cd (&Ufull)[4][4], const cd (&us)
       trw += wcol_s[p].r * tcol[p].r + wcol_s[p].i * tcol[p].i;
     }
     const double nW = qsum(nw);
-    const double cond = sqrt(nT) * sqrt(nW);  // ‖T‖_F ‖W‖_F >= cond_2(T)
-    if ((!pdc || !isfinite(cond) || cond > kCondLimitUA) && status == 0)
+    const double c2 = nT * nW;  // (‖T‖_F ‖W‖_F)² >= cond_2(T)²: no square roots
+    if ((!pdc || !isfinite(c2) || c2 > kCondLimitUA * kCondLimitUA) && status == 0)
       status = AMMMSE_STATUS_ILL_CONDITIONED;
-    if (pdc && status != AMMMSE_STATUS_NONFINITE) lndetw = lndet_diff4i(piva, pivc);  // pivc: inverse pivots
+    if (want_f && pdc && status != AMMMSE_STATUS_NONFINITE) lndetw = lndet_diff4i(piva, ipivc);
   } else {
     trw = s == 0 ? tcol[0].r : (s == 1 ? tcol[1].r : (s == 2 ? tcol[2].r : tcol[3].r));  // W = I
   }
-  fw = ak * (qsum(trw) - lndetw);
+  fw = want_f ? ak * (qsum(trw) - lndetw) : 0.0;
+}
+
+// K1 combine, product half: column s of P = α U W and D = −P T (the Ŷ factors of
+// objective.py:196-213).  pscr: 16 cd of per-user scratch.
+__device__ __forceinline__ void k1c_pd(const cd (&Ufull)[4][4], const cd (&us)[4], const cd (&tcol)[4],
+                                       const cd (&wcol_s)[4], double ak, bool weighted, int s, cd* pscr,
+                                       cd (&pcol)[4], cd (&dcol)[4]) {
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     cd acc = cmk(0.0);
@@ -310,17 +322,18 @@ __device__ __forceinline__ void k1c_quad(const cd (&Ufull)[4][4], const cd (&us)
 // every fp64 chain, and every cluster barrier flushes L1, where the spills
 // live); as separate functions they get their own allocation.  All operands
 // are shared-memory pointers.
-//   G planes: fp32, row stride ldg, the CTA's own columns; user kl (global
-//   k0 + kl) has its N x d diagonal block at rows 4 (k0 + kl), columns 4 kl.
+//   G: the own users' N x d diagonal blocks, fp32, addressed through QuadArgs
+//   strides (in place in a G plane, or a compact saved copy).
 //   gram: reduced Grams, 16 cd per GLOBAL user.  ucache / wcache: 16 cd per own user.
 // ---------------------------------------------------------------------------
 struct QuadArgs {
-  const float* Gr;
+  const float* Gr;  // diagonal blocks: element (own user kl, row p, column c) at Gr[kl * ustride + p * rstride + c]
   const float* Gi;
-  int ldg, k0, KL;
+  int ustride, rstride, k0, KL;
   const cd* gram;
   double sigma2;
   const double* alpha;
+  int want_f;  // compute the f_after_u / w / v terms and ln det W (they feed the trace only)
 };
 
 // WSR(t): rate[kl], fv[kl], ust2[kl] of the own users (one full warp)
@@ -340,25 +353,25 @@ static __device__ __noinline__ void wsr_users(QuadArgs q, const cd* ucache, cons
     const int kl = act ? kl0 + ul : 0;
     cd Tg[4][4], G[4][4], U[4][4], gs[4], us[4], ws[4];
     const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
-    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+    const size_t gbase = (size_t)kl * q.ustride;
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         Tg[p][c] = g[p * 4 + c];
-        G[p][c] = cmk((double)q.Gr[gbase + p * q.ldg + c], (double)q.Gi[gbase + p * q.ldg + c]);
+        G[p][c] = cmk((double)q.Gr[gbase + p * q.rstride + c], (double)q.Gi[gbase + p * q.rstride + c]);
         U[p][c] = ucache[kl * 16 + p * 4 + c];
       }
 #pragma unroll
     for (int p = 0; p < 4; ++p) {  // column sc (no dynamic register indexing)
-      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+      gs[p] = cmk((double)q.Gr[gbase + p * q.rstride + sc], (double)q.Gi[gbase + p * q.rstride + sc]);
       us[p] = ucache[kl * 16 + p * 4 + sc];
       ws[p] = wcache[kl * 16 + p * 4 + sc];
     }
     const double wss = wcache[kl * 16 + sc * 4 + sc].r;
     double rr, ff;
     int st;
-    wsr_quad(Tg, G, gs, q.sigma2, q.alpha[kl], U, us, ws, wss, lndetw[kl], sc, rr, ff, st);
+    wsr_quad(Tg, G, gs, q.sigma2, q.alpha[kl], U, us, ws, wss, lndetw[kl], sc, q.want_f != 0, rr, ff, st);
     if (act && sc == 0) {
       rate[kl] = rr;
       fv[kl] = ff;
@@ -380,8 +393,10 @@ struct K1Out4 {  // destinations of K1 (own users unless noted)
   double* scratch;   // kScratch doubles per own user
 };
 
-// K1(t+1), weight half (warp 2 of the block; pairs with k1_recv_users through
-// named barrier 1, 64 threads, once per pass of 8 users)
+// K1(t+1) in the weighted stage, warp 2: the weight half (W = I + Y^H Y), then — after
+// the named barrier 1 (64 threads, once per pass of 8 users) it shares with
+// k1_recv_users — the statistics half of the combine (ill-conditioning test,
+// ln det W, f_after_w) while warp 1 forms P and D.
 static __device__ __noinline__ void k1_weight_users(QuadArgs q, K1Out4 o) {
   const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
   for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
@@ -389,32 +404,47 @@ static __device__ __noinline__ void k1_weight_users(QuadArgs q, K1Out4 o) {
     const int kl = act ? kl0 + ul : 0;
     cd Tg[4][4], G[4][4], gs[4];
     const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
-    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+    const size_t gbase = (size_t)kl * q.ustride;
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         Tg[p][c] = g[p * 4 + c];
-        G[p][c] = cmk((double)q.Gr[gbase + p * q.ldg + c], (double)q.Gi[gbase + p * q.ldg + c]);
+        G[p][c] = cmk((double)q.Gr[gbase + p * q.rstride + c], (double)q.Gi[gbase + p * q.rstride + c]);
       }
 #pragma unroll
     for (int p = 0; p < 4; ++p)
-      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+      gs[p] = cmk((double)q.Gr[gbase + p * q.rstride + sc], (double)q.Gi[gbase + p * q.rstride + sc]);
     double* scr = o.scratch + (size_t)kl * kScratch;
-    double pivc[4];
+    cd* wcol = o.wcache + (size_t)kl * 16;
+    double ipivc[4];
     int pd;
-    k1w_quad(Tg, G, gs, q.sigma2, sc, reinterpret_cast<cd*>(scr), o.wcache + (size_t)kl * 16, pivc, pd);
-    if (sc == 0) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) scr[64 + j] = pivc[j];
-      scr[68] = (double)pd;
-    }
+    k1w_quad(Tg, G, gs, q.sigma2, sc, reinterpret_cast<cd*>(scr), wcol, ipivc, pd);
     asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    // warp 1 has left T (column sc), ‖T‖², the pivots of A and its status in the scratch
+    const cd* tsc = reinterpret_cast<const cd*>(scr + 64);
+    cd tcol[4], wcs[4];
+    double piva[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      tcol[p] = tsc[p * 4 + sc];
+      wcs[p] = wcol[p * 4 + sc];
+      piva[p] = scr[97 + p];
+    }
+    int st = (int)scr[101];
+    double fw_, lnw;
+    k1c_stat(tcol, scr[96], piva, wcs, ipivc, pd, q.alpha[kl], true, q.want_f != 0, sc, fw_, lnw, st);
+    if (act && sc == 0) {
+      o.lndetw[kl] = lnw;
+      o.fw[kl] = fw_;
+      o.ust[kl] = st;
+    }
   }
 }
 
-// K1(t+1), receiver half + combine (warp 1).  wprev / lndet_wprev: the previous
-// iteration's W bank (f_after_u, solvers.py:447).
+// K1(t+1), warp 1: the receiver half, then P = α U W and D = −P T.  In the weighted
+// stage the statistics half runs on warp 2 (k1_weight_users); otherwise (W = I) here.
+// wprev / lndet_wprev: the previous iteration's W bank (f_after_u, solvers.py:447).
 static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd* wprev, const double* lndet_wprev,
                                            bool weighted) {
   const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
@@ -423,12 +453,12 @@ static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd
     const int kl = act ? kl0 + ul : 0;
     cd Tg[4][4], gs[4], Wprow[4];
     const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
-    const size_t gbase = (size_t)(q.k0 + kl) * 4 * q.ldg + kl * 4;
+    const size_t gbase = (size_t)kl * q.ustride;
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
 #pragma unroll
       for (int c = 0; c <= p; ++c) Tg[p][c] = g[p * 4 + c];
-      gs[p] = cmk((double)q.Gr[gbase + p * q.ldg + sc], (double)q.Gi[gbase + p * q.ldg + sc]);
+      gs[p] = cmk((double)q.Gr[gbase + p * q.rstride + sc], (double)q.Gi[gbase + p * q.rstride + sc]);
       Wprow[p] = wprev[kl * 16 + sc * 4 + p];
     }
     double* scr = o.scratch + (size_t)kl * kScratch;
@@ -437,26 +467,36 @@ static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd
     cd Ufull[4][4], us[4], tcol[4];
     double fu_, nT, piva[4];
     int st;
-    k1u_quad(Tg, gs, q.sigma2, q.alpha[kl], Wprow, lndet_wprev[kl], sc, ucol, Ufull, us, tcol, fu_, nT, piva, st);
+    k1u_quad(Tg, gs, q.sigma2, q.alpha[kl], Wprow, lndet_wprev[kl], sc, q.want_f != 0, ucol, Ufull, us, tcol,
+             fu_, nT, piva, st);
     cd wcs[4];
-    double pivc[4] = {1.0, 1.0, 1.0, 1.0};
-    int pdc = 1;
     if (weighted) {
+      cd* tsc = reinterpret_cast<cd*>(scr + 64);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) tsc[p * 4 + sc] = tcol[p];
+      if (sc == 0) {
+        scr[96] = nT;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) scr[97 + j] = piva[j];
+        scr[101] = (double)st;
+      }
       asm volatile("bar.sync 1, 64;\n" ::: "memory");
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        wcs[p] = wcol[p * 4 + sc];
-        pivc[p] = scr[64 + p];
-      }
-      pdc = (int)scr[68];
+      for (int p = 0; p < 4; ++p) wcs[p] = wcol[p * 4 + sc];
     } else {
 #pragma unroll
       for (int p = 0; p < 4; ++p) wcs[p] = cmk(p == sc ? 1.0 : 0.0);
+      const double one[4] = {1.0, 1.0, 1.0, 1.0};
+      double fw_, lnw;
+      k1c_stat(tcol, nT, piva, wcs, one, 1, q.alpha[kl], false, q.want_f != 0, sc, fw_, lnw, st);
+      if (act && sc == 0) {
+        o.lndetw[kl] = lnw;
+        o.fw[kl] = fw_;
+        o.ust[kl] = st;
+      }
     }
     cd pcol[4], dcol[4];
-    double fw_, lnw;
-    k1c_quad(Ufull, us, tcol, nT, piva, wcs, pivc, pdc, q.alpha[kl], weighted, sc,
-             reinterpret_cast<cd*>(scr + 32), pcol, dcol, fw_, lnw, st);
+    k1c_pd(Ufull, us, tcol, wcs, q.alpha[kl], weighted, sc, reinterpret_cast<cd*>(scr + 32), pcol, dcol);
     if (act) {
 #pragma unroll
       for (int p = 0; p < 4; ++p) {  // row p, column sc
@@ -466,12 +506,7 @@ static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd
         o.Down[il] = make_float2((float)dcol[p].r, (float)dcol[p].i);
         if (!weighted) wcol[p * 4 + sc] = wcs[p];
       }
-      if (sc == 0) {
-        o.lndetw[kl] = lnw;
-        o.fu[kl] = fu_;
-        o.fw[kl] = fw_;
-        o.ust[kl] = st;
-      }
+      if (sc == 0) o.fu[kl] = fu_;
     }
   }
 }
