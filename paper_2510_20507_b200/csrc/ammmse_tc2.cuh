@@ -852,9 +852,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     xs[XS_FW] = sw;
     xs[XS_ST1] = st;
   };
-  auto k1_gather = [&]() {
+  auto k1_gather = [&](int first, int step) {
     const int per = NN * DD;
-    for (int i = tid; i < K * per; i += blockDim.x) {
+    for (int i = first; i < K * per; i += step) {
       const int owner = (i / per) / KL;
       if (owner != crank) {
         Uall[i] = cl.map_shared_rank(Uall, owner)[i];
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     if (tid == 0) k1_publish();
     cl.sync();
     xs_fetch();
-    k1_gather();
+    k1_gather(tid, blockDim.x);
   };
 
   // split store of one fp32 value of the B operand: rows n (hi) and n + 2 ncol (lo)
@@ -1278,6 +1278,24 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       }
       ctl.wn_next = stage_flag();
     };
+    // Results of K1(tn) from the local exchange copies (thread 0, after the xs_fetch
+    // that follows its publication): f_after_u / w sums and the first failure,
+    // i.e. update_weight_matrices raising inside iteration tn (solvers.py:455-460).
+    auto k1_status = [&](int tn, bool wn_k) {
+      ctl.f_u = xlsum(XS_FU);
+      ctl.f_w = xlsum(XS_FW);
+      const int st = xlfirst(XS_ST1);
+      if (st) {
+        if (!ctl.latched && wn_k) {
+          if (a.latch) ctl.latched = 1;
+          if (ctl.switch_it < 0) ctl.switch_it = tn;
+        }
+        ctl.status = st;
+        ctl.stop = 1;
+      }
+    };
+    if (tid == 0) k1_status(1, wn);
+    __syncthreads();
     // WSR of the own users from the reduced Gram gx[1] and the diagonal blocks
     // at (gr, gi): per-user rates / f_after_v, then the CTA partials -> exchange
     // slots.  One full warp.
@@ -1341,22 +1359,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     double power_p = 0.0, scale_p = 1.0;  // ‖X‖², scale of the pending iteration
     for (int t = 1; t <= a.max_iters; ++t) {
       const int bk = t & 1;  // bank holding K1(t)'s U / W / ln det W
-      if (tid == 0) {        // K1(t) results (published before the last cluster barrier)
-        ctl.f_u = xlsum(XS_FU);  // (local copies: xs_fetch after the publishing barrier)
-        ctl.f_w = xlsum(XS_FW);
-        const int st = xlfirst(XS_ST1);
-        if (st) {  // update_weight_matrices raised inside iteration t (solvers.py:455-460)
-          if (!ctl.latched && wn) {
-            if (a.latch) ctl.latched = 1;
-            if (ctl.switch_it < 0) ctl.switch_it = t;
-          }
-          ctl.status = st;
-          ctl.stop = 1;
-        }
-      }
       const bool extrap = (t >= 2) && (ctl.omega > 0.0);
-      __syncthreads();
       pc.mark(0);
+      // (the status of K1(t) was evaluated with the exchange fetch that followed it)
       if (ctl.stop && !pending) break;
       // (pending: the K1(t) failure belongs to a step that may still be discarded;
       // it is acted on after the state machine of t-1 below)
@@ -1451,7 +1456,6 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       pc.mark(15);
       if (more && tid == 32) k1_publish();
       cl.sync();
-      xs_fetch();
       pc.mark(5);
       if (a.itU) {  // block iterate of t (solvers.py:487-488), own users / columns
         const size_t it = (size_t)r * a.max_iters + (t - 1);
@@ -1481,13 +1485,25 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           }
         umma::fence_before();
       }
-      if (defer) {  // state machine of t postponed; the stage flag stays latched
+      // Warp 0: one batched read of the cluster's exchange slots, the state machine
+      // of t and the status of K1(t+1); the other warps meanwhile gather the other
+      // owners' U / α U W (valid when the speculated stage flag holds).
+      if (warp == 0) {
+        xs_fetch();
+        if (tid == 0) {
+          if (defer)
+            ctl.wn_next = 1;  // state machine of t postponed; the stage flag stays latched
+          else
+            state_machine(t, wn, power, scale);
+          if (more && (defer || !ctl.stop) && (ctl.wn_next != 0) == wn_spec) k1_status(t + 1, wn_spec);
+        }
+      } else if (more) {
+        k1_gather(tid - 32, blockDim.x - 32);
+      }
+      if (defer) {
         pending = true;
         power_p = power;
         scale_p = scale;
-        if (tid == 0) ctl.wn_next = 1;
-      } else if (tid == 0) {
-        state_machine(t, wn, power, scale);
       }
       __syncthreads();
       pc.mark(6);
@@ -1495,10 +1511,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       wn = ctl.wn_next != 0;
       if (more && wn != wn_spec) {  // mis-speculated stage flag: redo K1(t+1) (same inputs)
         k1_phase(GE, wn, true, bk, bk ^ 1);
-      } else if (more) {
-        k1_gather();
+        if (tid == 0) k1_status(t + 1, wn);
+        __syncthreads();
+        if (ctl.stop) break;
       }
-      __syncthreads();
       pc.mark(7);
     }
 
