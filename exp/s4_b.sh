@@ -11,6 +11,7 @@ cyc=1965e6*33/(v*it)
 ph=d['roofline'].get('bcgd_step',{}).get('phases')
 tot=sum(ph[:17])
 print('dbg $dbg', v, it, 'cycles/iter', cyc, d['config']['failed_realizations'])
-print([round(x/tot*cyc) for x in ph[:17]], 'K1 recv/weight per iter (CTA 0 only, x132):', [round(x/tot*cyc*132) for x in ph[17:19]])
+tot=sum(ph[:19])
+print([round(x/tot*cyc) for x in ph[:19]], 'producer-0 done-wait per iter (CTA 0, x132):', round(ph[19]/tot*cyc*132))
 PY
 done

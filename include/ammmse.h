@@ -116,10 +116,12 @@ typedef struct AmmmseOptions {
   int32_t h_placement; /* cluster engine only: 0 auto, 1 H resident in every CTA's SMEM,
                           2 H streamed from HBM/L2 through a cp.async ring, 3 streamed H and
                           the previous precoders in a per-CTA global scratch slot */
-  int32_t tensor_cores;/* cluster engine, complex64: 1 tcgen05 3xTF32 GEMMs (bulk-copied
-                          pre-split H planes, TMEM accumulators) where shape and shared memory
-                          allow; 2 FP32 FFMA GEMMs; 0 automatic (tensor cores for N = d = 4,
-                          where measured faster, else FFMA) */
+  int32_t tensor_cores;/* cluster engine, complex64: 0 automatic (N = d = 4: the second-generation
+                          tcgen05 engine, csrc/ammmse_tc2.cuh, where its shape rules hold — M = K N =
+                          128 as in BASELINE large — else the first-generation one; other N, d: FFMA,
+                          where measured faster); 1 first-generation tcgen05 3xTF32 GEMMs (bulk-copied
+                          pre-split H planes, TMEM accumulators) where shape and shared memory allow;
+                          2 FP32 FFMA GEMMs; 3 the second-generation engine or an error */
 } AmmmseOptions;
 
 /* SolveResult (solvers.py:174-182), struct-of-arrays.  Any pointer may be NULL. */

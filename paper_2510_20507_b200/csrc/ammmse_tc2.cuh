@@ -248,6 +248,7 @@ struct Pipe {
   uint32_t cm = 0, pm = 0, ever = 0;
   uint32_t call = 0;
   int dbg = 0;  // diagnostics (AMMMSE_PHASES builds): bit 0 skips the A copies, bit 1 the MMAs
+  unsigned long long* prof = nullptr;  // diagnostics: phase counters (AMMMSE_PHASES >= 2)
 };
 
 constexpr int kMmaWarp = 0, kMmaWarp2 = 2;  // (different SM sub-partitions)
@@ -309,7 +310,14 @@ __device__ __forceinline__ void gemm(Pipe& p, Clock& pc, const float* __restrict
       if (one_producer ? me == 0u : (c & 1u) == me) {
         const uint32_t fb = full0 + 8u * s, db = done0 + 8u * s, dst = stage_addr(s);
         // the stage's previous MMAs completed (done completion number fills - 1)
+#if AMMMSE_PHASES >= 2
+        const long long tw0 = clock64();
+#endif
         if (ever & bit) mbar_wait_spin_u32(db, ((pm >> s) & 1u) ^ 1u);
+#if AMMMSE_PHASES >= 2
+        if (p.prof && threadIdx.x == 32 && blockIdx.x == 0)
+          atomicAdd(p.prof + 19, (unsigned long long)(clock64() - tw0));
+#endif
         if (nocopy) {
           if (elect_one()) mbar_arrive_u32(fb);
         } else {
@@ -538,6 +546,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
   pipe.tmem = tc_tmem_slot;
 #if AMMMSE_PHASES
   pipe.dbg = a.dbg;
+  pipe.prof = a.prof;
   if (a.dbg) {  // ablation runs: defined (zero) operands and accumulators
     for (size_t i = tid; i < (size_t)tc2::kPerm * L.a_stage / 4; i += blockDim.x)
       reinterpret_cast<float*>(smem + L.oRing)[i] = 0.f;
@@ -705,9 +714,27 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           const double keep = up1 ? w[4 + e] : w[e];
           z[e] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
         }
-        const int idx0 = (up2 ? 8 : 0) + (up1 ? 4 : 0);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) gram_store<4>(k, idx0 + e, z[e], out);
+        // lane g holds packed sums 4 g .. 4 g + 3 (gram_pack order): store them into
+        // the full Hermitian 4 x 4 of user k
+        cd* G = out + (size_t)k * 16;
+        auto setre = [&](int p, int q, double v) {
+          G[p * 4 + q].r = v;
+          G[q * 4 + p].r = v;
+          if (p == q) G[p * 4 + p].i = 0.0;
+        };
+        auto setim = [&](int p, int q, double v) {
+          G[p * 4 + q].i = v;
+          G[q * 4 + p].i = -v;
+        };
+        if (g == 0) {
+          setre(0, 0, z[0]); setre(1, 0, z[1]); setre(1, 1, z[2]); setre(2, 0, z[3]);
+        } else if (g == 1) {
+          setre(2, 1, z[0]); setre(2, 2, z[1]); setre(3, 0, z[2]); setre(3, 1, z[3]);
+        } else if (g == 2) {
+          setre(3, 2, z[0]); setre(3, 3, z[1]); setim(1, 0, z[2]); setim(2, 0, z[3]);
+        } else {
+          setim(2, 1, z[0]); setim(3, 0, z[1]); setim(3, 1, z[2]); setim(3, 2, z[3]);
+        }
       }
     } else {
       gram_rows(Xr, Xi, out, first, nth);
@@ -1017,12 +1044,14 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
             ci[j] *= sc;
           }
         }
+        float pwb = 0.f;  // (32 squares per block in fp32, fp64 from there on)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           cr[j] -= st * gr[j];
           ci[j] -= st * gi[j];
-          pw += (double)cr[j] * (double)cr[j] + (double)ci[j] * (double)ci[j];
+          pwb = fmaf(cr[j], cr[j], fmaf(ci[j], ci[j], pwb));
         }
+        pw += (double)pwb;
         if (to_b) {
           emit_x(xo, t, q0, cr, ci);
         } else {
@@ -1378,8 +1407,16 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       pc.mark(10);
       const int xo = 1 - xc;
       double pw = epilogue_a(xc, xo, vsc(xc), vsc(xo), (float)ctl.step, (float)ctl.omega, extrap, true);
-      pw = block_sum(pw, red);  // (its barriers also order the B writes before the MMAs)
-      if (tid == 0) xs[XS_POWER] = pw;
+      // CTA partial of ‖X‖²: fixed shuffle tree, then thread 0 adds the warps in order
+      // (the barrier also orders the B writes before GEMM-B's MMAs)
+      pw = warp_allsum(pw);
+      if (lane == 0) red[warp] = pw;
+      __syncthreads();
+      if (tid == 0) {
+        double sp = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sp += red[w];
+        xs[XS_POWER] = sp;
+      }
       asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
       pc.mark(2);
       const bool more = t < a.max_iters;
@@ -1442,14 +1479,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
         if (!defer)
           wsr_warp(Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg, NN * ldg + DD, ldg, bk);
       } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
-#if AMMMSE_PHASES
-        const long long tk0 = clock64();
-#endif
         k1_pipelined(GE, wn_spec, bk, bk ^ 1);
-#if AMMMSE_PHASES
-        if (a.prof && (tid == 32 || tid == 64) && blockIdx.x == 0)
-          atomicAdd(a.prof + (tid == 32 ? 17 : 18), (unsigned long long)(clock64() - tk0));
-#endif
       }
       pc.mark(14);
       __syncthreads();
