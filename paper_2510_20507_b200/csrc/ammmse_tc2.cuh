@@ -622,9 +622,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     }
     return 0;
   };
-  auto gram_reduce = [&](int buf) {
+  auto gram_reduce = [&](int buf, int first, int step) {
     constexpr int per = NN * NN;
-    for (int i = tid; i < KL * per; i += blockDim.x) {
+    for (int i = first; i < KL * per; i += step) {
       const size_t gi = (size_t)k0 * per + i;
       cd s = cl.map_shared_rank(gx[buf], 0)[gi];
       for (int c = 1; c < C; ++c) s = cadd(s, cl.map_shared_rank(gx[buf], c)[gi]);
@@ -1249,7 +1249,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     bool wn = stage_flag();
     gram_rows(Gr[1], Gi[1], gx[0], tid, blockDim.x);
     cl.sync();
-    gram_reduce(0);
+    gram_reduce(0, tid, blockDim.x);
     __syncthreads();
     k1_phase(1, wn, true, 0, 1);
     pc.mark(9);
@@ -1471,8 +1471,14 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       pc.mark(12);
       cl.sync();
       pc.mark(13);
-      gram_reduce(1);
-      if (more) gram_reduce(0);
+      if (more) {  // both Grams at once: one DSMEM round trip
+        if (tid < 128)
+          gram_reduce(1, tid, 128);
+        else
+          gram_reduce(0, tid - 128, 128);
+      } else {
+        gram_reduce(1, tid, blockDim.x);
+      }
       __syncthreads();
       pc.mark(4);
       if (tid < 32) {  // warp 0: WSR(t) unless deferred
@@ -1580,7 +1586,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       __syncthreads();
       gram_rows(Gr[GE], Gi[GE], gx[0], tid, blockDim.x);
       cl.sync();
-      gram_reduce(0);
+      gram_reduce(0, tid, blockDim.x);
       __syncthreads();
       k1_phase(GE, weighted, false, 0, 0);
       int st = xfirst(XS_ST1);
