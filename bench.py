@@ -507,7 +507,8 @@ def main():
         "work": f"F=16*K^2*N*d*M={fpu:.0f} flop per realization-iteration x {iters_total} "
                 f"realization-iterations per launch (whole solve counted at GEMM flops)",
         "kernel": f"{kname} (1 launch per step)",
-        "gemm_step": "bench_gemmstep.py / profiles/r02_gemmstep.md: the GEMM step alone",
+        "gemm_step": "profiles/r02_summary.md: per-phase cycles of the tc2 kernel; bench_gemmstep.py: the "
+                     "first-generation GEMM step alone",
     })
 
     # BCGD-step share of the kernel (GEMM-step fraction =
