@@ -113,9 +113,12 @@ struct T2Layout {
     if (NN == 4 && DD == 4) return (size_t)KL * quad::kScratch;  // quad-lane K1 (user_algebra_quad.cuh)
     return (NN == 2 && DD == 2) ? 0 : (size_t)KL * (2 * DD * DD + NN + 1);
   }
+  __host__ __device__ size_t wsr_count() const {
+    return (NN == 4 && DD == 4) ? (size_t)KL * quad::kWsrScratch : 0;  // two-warp WSR (wsr_users_a / _c)
+  }
   __host__ __device__ size_t dbl_count() const {
     return (size_t)2 * 2 * K * NN * NN + 2 * 2 * KL * NN * DD + 2 * 2 * KL * DD * DD + 9 * KL +
-           XS_COUNT + k1w_count() + 32;
+           XS_COUNT + k1w_count() + wsr_count() + 32;
   }
 };
 
@@ -518,6 +521,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
   double* ust2 = dp; dp += KL;
   double* xs = dp; dp += XS_COUNT;
   double* k1w = dp; dp += L.k1w_count();
+  double* wsrw = dp; dp += L.wsr_count();
   double* red = dp;
 
   // ---- pipeline setup: mbarriers, TMEM ----
@@ -672,7 +676,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           for (int q = 0; q < 4; ++q) sr[p][q] = si[p][q] = 0.0;
         const R* xr = Xr + (size_t)k * 4 * ldg;
         const R* xi = Xi + (size_t)k * 4 * ldg;
-#pragma unroll 2
+#pragma unroll 1  // (compact body: the loop then runs out of the L0 instruction cache)
         for (int j = g; j < ncol; j += 4) {
           double gr[4], gi[4];
 #pragma unroll
@@ -1328,12 +1332,16 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     // WSR of the own users from the reduced Gram gx[1] and the diagonal blocks
     // at (gr, gi): per-user rates / f_after_v, then the CTA partials -> exchange
     // slots.  One full warp.
-    auto wsr_warp = [&](const R* gr, const R* gi, int ustride, int rstride, int bank) {
+    // split: warp 3 factors the interference matrices meanwhile (wsr_c_warp below)
+    auto wsr_warp = [&](const R* gr, const R* gi, int ustride, int rstride, int bank, bool split) {
       const cd* ucache = ucb[bank];
       const cd* wcache = wcb[bank];
       if constexpr (NN == 4 && DD == 4) {  // four lanes per user (user_algebra_quad.cuh)
         const quad::QuadArgs qa{gr, gi, ustride, rstride, k0, KL, gx[1], ctl.sigma2, alpha, a.trace != nullptr};
-        quad::wsr_users(qa, ucache, wcache, lndb[bank], rate, fv, ust2);
+        if (split)
+          quad::wsr_users_a(qa, ucache, wcache, lndb[bank], wsrw, rate, fv, ust2);
+        else
+          quad::wsr_users(qa, ucache, wcache, lndb[bank], rate, fv, ust2);
       } else {
         for (int kl = lane; kl < KL; kl += 32) {
           cd Tg[NN][NN], Gkk[NN][DD], U[NN][DD], W[DD][DD];
@@ -1400,7 +1408,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       // ∇ = H^H Ŷ  (deferred mode: WSR(t-1) on the side warp meanwhile)
       if (pending) {
         tc2::gemm(pipe, pc, hpA, nchA, ncol, nsets, hpB,
-                  [&]() { wsr_warp(gkk_save, gkk_save + KL * NN * DD, NN * DD, DD, (t - 1) & 1); });
+                  [&]() { wsr_warp(gkk_save, gkk_save + KL * NN * DD, NN * DD, DD, (t - 1) & 1, false); });
       } else {
         tc2::gemm(pipe, pc, hpA, nchA, ncol, nsets, hpB);
       }
@@ -1481,10 +1489,20 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       }
       __syncthreads();
       pc.mark(4);
-      if (tid < 32) {  // warp 0: WSR(t) unless deferred
+      constexpr bool kQuad = NN == 4 && DD == 4;
+      if (tid < 32) {  // warp 0: WSR(t) unless deferred (with warp 3 for N = d = 4)
         if (!defer)
-          wsr_warp(Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg, NN * ldg + DD, ldg, bk);
-      } else if (more) {  // warps 1..: K1(t+1) with the speculated stage flag
+          wsr_warp(Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg, NN * ldg + DD, ldg, bk,
+                   kQuad);
+      } else if (kQuad && warp == 3) {
+        if constexpr (kQuad) {
+          if (!defer) {
+            const quad::QuadArgs qa{Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg,
+                                    NN * ldg + DD, ldg, k0, KL, gx[1], ctl.sigma2, alpha, a.trace != nullptr};
+            quad::wsr_users_c(qa, wsrw);
+          }
+        }
+      } else if (more) {  // warps 1, 2: K1(t+1) with the speculated stage flag
         k1_pipelined(GE, wn_spec, bk, bk ^ 1);
       }
       pc.mark(14);

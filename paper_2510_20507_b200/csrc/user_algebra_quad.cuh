@@ -380,6 +380,138 @@ static __device__ __noinline__ void wsr_users(QuadArgs q, const cd* ucache, cons
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// WSR(t) split over two warps (the rate needs two independent 4 x 4 Cholesky
+// factorisations per user, A = T + σ² I and C = A − G G^H, each a chain of
+// dependent fp64 operations): warp "A" factors A (and forms the f_after_v term
+// when a trace is recorded), warp "C" forms G G^H — row s on lane s, exchanged
+// through the scratch — and factors C; they meet at named barrier 2 (64 threads)
+// once per pass of 8 users and warp A finishes the rate.
+//   wscr: kWsrScratch doubles per own user.
+// ---------------------------------------------------------------------------
+constexpr int kWsrScratch = 40;  // G G^H rows (16 cd), inverse pivots of C (4), ok flag
+
+static __device__ __noinline__ void wsr_users_c(QuadArgs q, double* wscr) {
+  const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
+  for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
+    const bool act = kl0 + ul < q.KL;
+    const int kl = act ? kl0 + ul : 0;
+    const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
+    const size_t gbase = (size_t)kl * q.ustride;
+    cd G[4][4], grow[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        G[p][c] = cmk((double)q.Gr[gbase + p * q.rstride + c], (double)q.Gi[gbase + p * q.rstride + c]);
+      grow[p] = cmk((double)q.Gr[gbase + sc * q.rstride + p], (double)q.Gi[gbase + sc * q.rstride + p]);
+    }
+    double* scr = wscr + (size_t)kl * kWsrScratch;
+    cd* orow = reinterpret_cast<cd*>(scr);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {  // (G G^H)[sc][b]
+      cd o = cmk(0.0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o = cadd(o, cmulcb(grow[c], G[b][c]));
+      orow[sc * 4 + b] = o;
+    }
+    __syncwarp();
+    cd L[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) L[a][b] = csub(g[a * 4 + b], orow[a * 4 + b]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      L[a][a].r += q.sigma2;
+      L[a][a].i = 0.0;
+    }
+    double ic[4];
+    const bool ok = chol4_inv(L, ic);
+    if (sc == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) scr[32 + j] = ic[j];
+      scr[36] = ok ? 1.0 : 0.0;
+    }
+    asm volatile("bar.sync 2, 64;\n" ::: "memory");
+  }
+}
+
+static __device__ __noinline__ void wsr_users_a(QuadArgs q, const cd* ucache, const cd* wcache,
+                                                const double* lndetw, const double* wscr, double* rate,
+                                                double* fv, double* ust2) {
+  const int lane = threadIdx.x & 31, ul = lane >> 2, sc = lane & 3;
+  for (int kl0 = 0; kl0 < q.KL; kl0 += 8) {
+    const bool act = kl0 + ul < q.KL;
+    const int kl = act ? kl0 + ul : 0;
+    const cd* g = q.gram + (size_t)(q.k0 + kl) * 16;
+    const size_t gbase = (size_t)kl * q.ustride;
+    cd Tg[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) Tg[p][c] = g[p * 4 + c];
+    double ff = 0.0;
+    if (q.want_f) {  // f_after_v (trace only): Tr W + Re Σ conj(UW) ∘ (A U − 2 G), column sc
+      cd U[4][4], gs[4], us[4], ws[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) U[p][c] = ucache[kl * 16 + p * 4 + c];
+        gs[p] = cmk((double)q.Gr[gbase + p * q.rstride + sc], (double)q.Gi[gbase + p * q.rstride + sc]);
+        us[p] = ucache[kl * 16 + p * 4 + sc];
+        ws[p] = wcache[kl * 16 + p * 4 + sc];
+      }
+      double term = wcache[kl * 16 + sc * 4 + sc].r;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        cd x = cscale(us[a], q.sigma2), y = cmk(0.0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          cfma(x, Tg[a][b], us[b]);
+          cfma(y, U[a][b], ws[b]);
+        }
+        const cd z = cmk(x.r - 2.0 * gs[a].r, x.i - 2.0 * gs[a].i);
+        term += y.r * z.r + y.i * z.i;  // Re(conj(uw) z)
+      }
+      ff = q.alpha[kl] * (qsum(term) - lndetw[kl]);
+    }
+    cd L[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) L[a][b] = Tg[a][b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      L[a][a].r += q.sigma2;
+      L[a][a].i = 0.0;
+    }
+    double ia[4], pa[4], ic[4];
+    const bool okA = chol4_inv(L, ia);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pa[j] = L[j][j].r;
+    asm volatile("bar.sync 2, 64;\n" ::: "memory");
+    const double* scr = wscr + (size_t)kl * kWsrScratch;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ic[j] = scr[32 + j];
+    const bool ok = okA && scr[36] != 0.0;
+    double rr = 0.0;
+    int st = 0;
+    if (ok) {
+      const double r = lndet_diff4i(pa, ic);
+      rr = q.alpha[kl] * (r > 0.0 ? r : 0.0);
+    } else {
+      st = AMMMSE_STATUS_NONFINITE;
+    }
+    if (act && sc == 0) {
+      rate[kl] = rr;
+      fv[kl] = ff;
+      ust2[kl] = st;
+    }
+  }
+}
+
 struct K1Out4 {  // destinations of K1 (own users unless noted)
   cd* ucache;        // 16 cd per user
   cd* wcache;        // 16 cd per user
