@@ -422,6 +422,8 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
      // BASELINE large (K1(t+1) is as long as WSR(t), so hiding WSR alone does not pay).
     const char* de = getenv("AMMMSE_TC2_DEFER");
     a.tc_defer = (de && de[0] == '1') ? 1 : 0;
+    const char* ws = getenv("AMMMSE_TC2_WSR_SPLIT");  // A/B knob: 0 keeps WSR(t) on one warp
+    a.tc_wsr_split = !(ws && ws[0] == '0');
   }
   if (a.tcm) {  // H planes after the V_old slots, 256-byte aligned
     int sms2 = 0;

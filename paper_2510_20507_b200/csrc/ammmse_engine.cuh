@@ -89,6 +89,7 @@ struct EngineArgs {
   int tc_stages;           // tcm == 2 (ammmse_tc2.cuh): A ring depth
   int dbg;                 // diagnostic builds: ablation bits (AMMMSE_DBG)
   int tc_defer;            // tcm == 2: WSR(t) deferred into GEMM-A(t+1) once the stage is latched
+  int tc_wsr_split;        // tcm == 2: WSR(t) on two warps (A / C factorisations concurrently)
   unsigned long long* prof;  // debug: per-phase clock64 totals (nullptr = off)
   long long B;
   unsigned long long* counter;

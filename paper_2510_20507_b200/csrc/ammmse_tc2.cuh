@@ -74,7 +74,7 @@ struct T2Layout {
   int acc_cols;  // TMEM columns of the accumulators; the precoders, then G_old follow
   int v_cols;
   size_t nG;     // floats per G plane
-  size_t oRing, oB, oG0, oG1, oU, oP, oD, oGk, dbl_off, bytes;  // byte offsets
+  size_t oRing, oB, oG0, oG1, oP, oD, oGk, dbl_off, bytes;  // byte offsets
 
   __host__ __device__ void init(int M_, int K_, int C_, int S_) {
     M = M_;
@@ -100,9 +100,8 @@ struct T2Layout {
     oG0 = oB + (size_t)(rows / KW) * b_chunk;
     oG0 = (oG0 + 15) & ~(size_t)15;
     oG1 = oG0 + 2 * nG * 4;
-    oU = (oG1 + 2 * nG * 4 + 15) & ~(size_t)15;  // RC<float>[K*NN*DD]
-    oP = oU + (size_t)K * NN * DD * 8;
-    oD = oP + (size_t)K * NN * DD * 8;           // RC<float>[KL*NN*DD]
+    oP = (oG1 + 2 * nG * 4 + 15) & ~(size_t)15;  // RC<float>[K*NN*NN]: M_k = α U W U^H of every user
+    oD = oP + (size_t)K * NN * NN * 8;           // RC<float>[KL*NN*DD]
     oGk = oD + (size_t)KL * NN * DD * 8;         // float[2][KL*NN*DD]: saved diagonal blocks of G_new
     dbl_off = (oGk + (size_t)KL * NN * DD * 8 + 15) & ~(size_t)15;
     bytes = dbl_off + dbl_count() * sizeof(double);
@@ -497,8 +496,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
   float* Gi[2];
   Gr[0] = reinterpret_cast<float*>(smem + L.oG0); Gi[0] = Gr[0] + L.nG;
   Gr[1] = reinterpret_cast<float*>(smem + L.oG1); Gi[1] = Gr[1] + L.nG;
-  RC<R>* Uall = reinterpret_cast<RC<R>*>(smem + L.oU);
-  RC<R>* Pall = reinterpret_cast<RC<R>*>(smem + L.oP);
+  // Ŷ factor of every user: M_k = P_k U_k^H = α_k U_k W_k U_k^H (N x N), so that the
+  // off-diagonal blocks are Ŷ_kj = M_k Ĝ_kj (objective.py:196-213 in factored form)
+  RC<R>* Mall = reinterpret_cast<RC<R>*>(smem + L.oP);
   RC<R>* Down = reinterpret_cast<RC<R>*>(smem + L.oD);
   unsigned char* bfull = smem + L.oB;
   float* gkk_save = reinterpret_cast<float*>(smem + L.oGk);
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           for (int q = 0; q < 4; ++q) sr[p][q] = si[p][q] = 0.0;
         const R* xr = Xr + (size_t)k * 4 * ldg;
         const R* xi = Xi + (size_t)k * 4 * ldg;
-#pragma unroll 1  // (compact body: the loop then runs out of the L0 instruction cache)
+#pragma unroll 2
         for (int j = g; j < ncol; j += 4) {
           double gr[4], gi[4];
 #pragma unroll
@@ -774,11 +774,18 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     for (int p = 0; p < NN; ++p)
 #pragma unroll
       for (int q = 0; q < DD; ++q) {
-        const int ig = ((k0 + kl) * NN + p) * DD + q, il = (kl * NN + p) * DD + q;
-        Uall[ig] = RC<R>{(R)o.U[p][q].r, (R)o.U[p][q].i};
-        Pall[ig] = RC<R>{(R)o.P[p][q].r, (R)o.P[p][q].i};
+        const int il = (kl * NN + p) * DD + q;
         Down[il] = RC<R>{(R)o.D[p][q].r, (R)o.D[p][q].i};
         ucache[il] = o.U[p][q];
+      }
+#pragma unroll
+    for (int p = 0; p < NN; ++p)
+#pragma unroll
+      for (int b = 0; b < NN; ++b) {  // M = P U^H
+        cd acc = cmk(0.0);
+#pragma unroll
+        for (int q = 0; q < DD; ++q) acc = cadd(acc, cmulcb(o.P[p][q], o.U[b][q]));
+        Mall[((k0 + kl) * NN + p) * NN + b] = RC<R>{(R)acc.r, (R)acc.i};
       }
 #pragma unroll
     for (int p = 0; p < DD; ++p)
@@ -810,8 +817,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       const quad::QuadArgs qa{Gr[gsrc] + (size_t)k0 * NN * ldg, Gi[gsrc] + (size_t)k0 * NN * ldg,
                               NN * ldg + DD, ldg, k0, KL, gx[0], ctl.sigma2, alpha, a.trace != nullptr};
       const quad::K1Out4 ko{ucb[bout], wcb[bout], lndb[bout], fu, fw, ust,
-                            reinterpret_cast<float2*>(Uall), reinterpret_cast<float2*>(Pall),
-                            reinterpret_cast<float2*>(Down), k1w};
+                            reinterpret_cast<float2*>(Mall), reinterpret_cast<float2*>(Down), k1w};
       if (warp == 2)
         quad::k1_weight_users(qa, ko);
       else
@@ -884,13 +890,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
     xs[XS_ST1] = st;
   };
   auto k1_gather = [&](int first, int step) {
-    const int per = NN * DD;
+    const int per = NN * NN;
     for (int i = first; i < K * per; i += step) {
       const int owner = (i / per) / KL;
-      if (owner != crank) {
-        Uall[i] = cl.map_shared_rank(Uall, owner)[i];
-        Pall[i] = cl.map_shared_rank(Pall, owner)[i];
-      }
+      if (owner != crank) Mall[i] = cl.map_shared_rank(Mall, owner)[i];
     }
   };
   auto k1_phase = [&](int gsrc, bool weighted, bool want_f, int bin, int bout) {
@@ -929,32 +932,20 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
           yi[p] = v.i;
         }
       } else {
-        R gr[NN], gi[NN], qr[DD], qi[DD];
+        R gr[NN], gi[NN];
 #pragma unroll
         for (int p = 0; p < NN; ++p) {
           gr[p] = Yr[(m * NN + p) * ldg + jl];
           gi[p] = Yi[(m * NN + p) * ldg + jl];
         }
 #pragma unroll
-        for (int q = 0; q < DD; ++q) {
-          R sr = 0, si = 0;
-#pragma unroll
-          for (int p = 0; p < NN; ++p) {
-            const RC<R> u = Uall[(m * NN + p) * DD + q];
-            sr = fma(u.r, gr[p], fma(u.i, gi[p], sr));
-            si = fma(u.r, gi[p], fma(-u.i, gr[p], si));
-          }
-          qr[q] = sr;
-          qi[q] = si;
-        }
-#pragma unroll
         for (int p = 0; p < NN; ++p) {
           R sr = 0, si = 0;
 #pragma unroll
-          for (int q = 0; q < DD; ++q) {
-            const RC<R> pp = Pall[(m * NN + p) * DD + q];
-            sr = fma(pp.r, qr[q], fma(-pp.i, qi[q], sr));
-            si = fma(pp.r, qi[q], fma(pp.i, qr[q], si));
+          for (int b = 0; b < NN; ++b) {
+            const RC<R> mm = Mall[(m * NN + p) * NN + b];
+            sr = fma(mm.r, gr[b], fma(-mm.i, gi[b], sr));
+            si = fma(mm.r, gi[b], fma(mm.i, gr[b], si));
           }
           yr[p] = sr;
           yi[p] = si;
@@ -1490,11 +1481,12 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
       __syncthreads();
       pc.mark(4);
       constexpr bool kQuad = NN == 4 && DD == 4;
+      const bool wsplit = kQuad && a.tc_wsr_split;
       if (tid < 32) {  // warp 0: WSR(t) unless deferred (with warp 3 for N = d = 4)
         if (!defer)
           wsr_warp(Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg, NN * ldg + DD, ldg, bk,
-                   kQuad);
-      } else if (kQuad && warp == 3) {
+                   wsplit);
+      } else if (wsplit && warp == 3) {
         if constexpr (kQuad) {
           if (!defer) {
             const quad::QuadArgs qa{Gr[GN] + (size_t)k0 * NN * ldg, Gi[GN] + (size_t)k0 * NN * ldg,

@@ -519,8 +519,7 @@ struct K1Out4 {  // destinations of K1 (own users unless noted)
   double* fu;
   double* fw;
   double* ust;
-  float2* Uall;      // fp32, 16 per GLOBAL user
-  float2* Pall;      // fp32, 16 per GLOBAL user
+  float2* Mall;      // fp32, 16 per GLOBAL user: M = P U^H = α U W U^H
   float2* Down;      // fp32, 16 per own user
   double* scratch;   // kScratch doubles per own user
 };
@@ -628,13 +627,17 @@ static __device__ __noinline__ void k1_recv_users(QuadArgs q, K1Out4 o, const cd
       }
     }
     cd pcol[4], dcol[4];
+    const cd* pscr_c = reinterpret_cast<const cd*>(scr + 32);
     k1c_pd(Ufull, us, tcol, wcs, q.alpha[kl], weighted, sc, reinterpret_cast<cd*>(scr + 32), pcol, dcol);
     if (act) {
 #pragma unroll
       for (int p = 0; p < 4; ++p) {  // row p, column sc
         const int ig = ((q.k0 + kl) * 4 + p) * 4 + sc, il = (kl * 4 + p) * 4 + sc;
-        o.Uall[ig] = make_float2((float)us[p].r, (float)us[p].i);
-        o.Pall[ig] = make_float2((float)pcol[p].r, (float)pcol[p].i);
+        // column sc of M = P U^H: M[p][sc] = Σ_c P[p][c] conj(U[sc][c]) (P full in the scratch)
+        cd mm = cmk(0.0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mm = cadd(mm, cmulcb(pscr_c[p * 4 + c], ucol[sc * 4 + c]));
+        o.Mall[ig] = make_float2((float)mm.r, (float)mm.i);
         o.Down[il] = make_float2((float)dcol[p].r, (float)dcol[p].i);
         if (!weighted) wcol[p * 4 + sc] = wcs[p];
       }
