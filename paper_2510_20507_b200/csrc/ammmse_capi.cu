@@ -422,8 +422,11 @@ int ammmse_solve(const AmmmseDims* dims, const AmmmseProblem* prob, const Ammmse
      // BASELINE large (K1(t+1) is as long as WSR(t), so hiding WSR alone does not pay).
     const char* de = getenv("AMMMSE_TC2_DEFER");
     a.tc_defer = (de && de[0] == '1') ? 1 : 0;
-    const char* ws = getenv("AMMMSE_TC2_WSR_SPLIT");  // A/B knob: 0 keeps WSR(t) on one warp
-    a.tc_wsr_split = !(ws && ws[0] == '0');
+    // A/B knob: AMMMSE_TC2_WSR_SPLIT=1 runs WSR(t) on two warps (A / C factorisations
+    // concurrently).  Off by default: measured 2 158 vs 2 212 realizations/s (K1(t+1) on
+    // warps 1-2 bounds the phase; the extra warp and named barrier only add contention).
+    const char* ws = getenv("AMMMSE_TC2_WSR_SPLIT");
+    a.tc_wsr_split = (ws && ws[0] == '1') ? 1 : 0;
   }
   if (a.tcm) {  // H planes after the V_old slots, 256-byte aligned
     int sms2 = 0;

@@ -99,6 +99,22 @@ def test_tc2_deferred_wsr_mode_is_identical(cuda, monkeypatch):
     np.testing.assert_allclose(inline.stationarity_residual, deferred.stationarity_residual, rtol=1e-4)
 
 
+def test_tc2_two_warp_wsr_is_identical(cuda, monkeypatch):
+    """AMMMSE_TC2_WSR_SPLIT=1 factors A and C of every user on two warps concurrently (same
+    arithmetic per factorisation): identical iteration counts and precoders, WSR to fp64 rounding."""
+    b = build_batch(LARGE["M"], LARGE["N"], LARGE["K"], LARGE["d"], 5, p_max=100.0, weights="uniform",
+                    dtype=np.complex64, seed0=19)
+    opts = SolverOptions(algorithm="ammmse", gamma=0.002, omega=0.8, eps2=1e-5, max_iters=120)
+    monkeypatch.setenv("AMMMSE_TC2_WSR_SPLIT", "0")
+    one = _run(b, opts, record_trace=True, tensor_cores=3)
+    monkeypatch.setenv("AMMMSE_TC2_WSR_SPLIT", "1")
+    two = _run(b, opts, record_trace=True, tensor_cores=3)
+    np.testing.assert_array_equal(one.iterations, two.iterations)
+    np.testing.assert_array_equal(one.final_precoders, two.final_precoders)
+    np.testing.assert_allclose(one.wsr_bits, two.wsr_bits, rtol=1e-12)
+    np.testing.assert_allclose(one.trace[:, :, 1:8], two.trace[:, :, 1:8], rtol=1e-9, atol=1e-12)
+
+
 @pytest.mark.parametrize("kw", [dict(max_iters=1), dict(max_iters=2), dict(omega=0.0, max_iters=40),
                                 dict(eps1=1e-12, eps2=1e-13, max_iters=30),  # never leaves stage I
                                 dict(eps1=10.0, eps2=1e-5, max_iters=40)])   # weighted from t = 2
