@@ -112,7 +112,8 @@ def test_tc2_two_warp_wsr_is_identical(cuda, monkeypatch):
     np.testing.assert_array_equal(one.iterations, two.iterations)
     np.testing.assert_array_equal(one.final_precoders, two.final_precoders)
     np.testing.assert_allclose(one.wsr_bits, two.wsr_bits, rtol=1e-12)
-    np.testing.assert_allclose(one.trace[:, :, 1:8], two.trace[:, :, 1:8], rtol=1e-9, atol=1e-12)
+    n = int(one.iterations.min())
+    np.testing.assert_allclose(one.trace[:, :n, 1:8], two.trace[:, :n, 1:8], rtol=1e-9, atol=1e-12)
 
 
 @pytest.mark.parametrize("kw", [dict(max_iters=1), dict(max_iters=2), dict(omega=0.0, max_iters=40),

@@ -164,6 +164,25 @@ class TestCAbi:
         assert h.ammmse_check_dims(D(4, 64, 2, 16, 5, 0)) == _native.ERR_UNSUPPORTED
         assert "invalid" in _native.error_string(_native.ERR_INVALID)
 
+    def test_planner_engine_choice(self):
+        """ammmse_plan_info (no GPU needed): BASELINE large runs on the second-generation
+        tensor-core engine (tensor_cores == 2) within the sm_100 shared-memory limit, the other
+        BASELINE shapes keep their engines, and forcing tc2 on a shape outside its rules fails."""
+        D, O = _native.AmmmseDims, _native.AmmmseOptions
+        large = _native.plan_info(D(64, 128, 4, 32, 4, 0), O(max_iters=10))
+        assert large["tensor_cores"] == 2 and large["cluster"] == 4 and large["threads"] == 256
+        assert large["smem_bytes"] <= 232448 - 2048  # static shared (control block, barriers, slots)
+        assert _native.plan_info(D(64, 128, 4, 32, 4, 0), O(max_iters=10, tensor_cores=2))["tensor_cores"] == 0
+        assert _native.plan_info(D(64, 128, 4, 32, 4, 0), O(max_iters=10, tensor_cores=1))["tensor_cores"] == 1
+        medium = _native.plan_info(D(64, 64, 2, 16, 2, 0), O(max_iters=10))
+        assert medium["cluster"] == 0 and medium["tensor_cores"] == 0
+        massive = _native.plan_info(D(64, 256, 2, 64, 2, 0), O(max_iters=10))
+        assert massive["cluster"] == 4 and massive["tensor_cores"] == 0
+        with pytest.raises(Exception):
+            _native.plan_info(D(64, 256, 2, 64, 2, 0), O(max_iters=10, tensor_cores=3))
+        # complex128 never takes a tensor-core engine
+        assert _native.plan_info(D(8, 128, 4, 32, 4, 1), O(max_iters=10))["tensor_cores"] == 0
+
     def test_solve_rejects_null_problem_without_touching_gpu(self):
         h = _native.lib()
         d = _native.AmmmseDims(4, 64, 2, 16, 2, 0)
