@@ -465,6 +465,72 @@ __device__ __forceinline__ void load_acc(const Pipe& p, uint32_t lane_base, int 
   }
 }
 
+// Largest eigenvalue of a Hermitian n x n matrix by the cyclic Jacobi method of
+// herm_eig_max (small_linalg.cuh: same rotations in the same order on the 2n x 2n
+// real embedding), run by a whole warp on a matrix in shared memory: lane r
+// updates row / column entry r of each rotation.  The one-thread version keeps
+// the 8 x 8 matrix in local memory (dynamic indices) and costs ~1 M cycles per
+// user; this one a few 10 k.  A: identical in every lane; S: 4 n² doubles of
+// shared scratch of this warp.
+template <int n>
+__device__ __forceinline__ double herm_eig_max_warp(const cd (&A)[n][n], double* S, int lane) {
+  if (n == 1) return A[0][0].r;
+  constexpr int m = 2 * n;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int j = 0; j < n; ++j) {
+        const double re = 0.5 * (A[i][j].r + A[j][i].r);  // hermitianize (linalg.py:12-14)
+        const double im = 0.5 * (A[i][j].i - A[j][i].i);
+        S[i * m + j] = re;
+        S[(i + n) * m + j + n] = re;
+        S[(i + n) * m + j] = im;
+        S[i * m + j + n] = -im;
+      }
+  }
+  __syncwarp();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int done = 0;
+    if (lane == 0) {  // same summation order as the one-thread version
+      double off = 0.0, diag = 0.0;
+      for (int p = 0; p < m; ++p) {
+        diag += S[p * m + p] * S[p * m + p];
+        for (int q = p + 1; q < m; ++q) off += S[p * m + q] * S[p * m + q];
+      }
+      done = (off <= 1e-34 * diag || off == 0.0) ? 1 : 0;
+    }
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = S[p * m + q];
+        if (apq == 0.0) continue;  // (uniform: every lane reads the same element)
+        const double theta = (S[q * m + q] - S[p * m + p]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0);
+        const double s = t * c;
+        __syncwarp();  // the reads above precede the updates
+        if (lane < m) {  // columns p, q
+          const double srp = S[lane * m + p], srq = S[lane * m + q];
+          S[lane * m + p] = c * srp - s * srq;
+          S[lane * m + q] = s * srp + c * srq;
+        }
+        __syncwarp();
+        if (lane < m) {  // rows p, q
+          const double spr = S[p * m + lane], sqr = S[q * m + lane];
+          S[p * m + lane] = c * spr - s * sqr;
+          S[q * m + lane] = s * spr + c * sqr;
+        }
+        __syncwarp();
+      }
+  }
+  double mx = S[0];
+  for (int p = 1; p < m; ++p) mx = fmax(mx, S[p * m + p]);
+  __syncwarp();
+  return mx;
+}
+
 }  // namespace tc2
 
 template <int NN, int DD>
@@ -1205,7 +1271,13 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) ammmse_tc2_kernel(EngineArgs
         cd G[NN][NN];
         for (int p = 0; p < NN; ++p)
           for (int q = 0; q < NN; ++q) G[p][q] = cmk(warp_allsum(sr[p][q]), warp_allsum(si[p][q]));
-        if (lane == 0) rate[kl] = herm_eig_max<NN>(G);
+        // (scratch: the K1 exchange region, idle during the setup; 4 N² doubles per warp)
+        double lam;
+        if ((size_t)(blockDim.x >> 5) * 4 * NN * NN <= L.k1w_count())
+          lam = tc2::herm_eig_max_warp<NN>(G, k1w + (size_t)warp * 4 * NN * NN, lane);
+        else
+          lam = herm_eig_max<NN>(G);
+        if (lane == 0) rate[kl] = lam;
       }
       __syncthreads();
       if (tid == 0) {
