@@ -128,7 +128,7 @@ int make_plan(const AmmmseDims* d, int force_c, int h_placement, int tensor_core
       if (mi == 0 && d->dtype == AMMMSE_COMPLEX64 && e->cluster_solve_tc2 && h_placement == 0 &&
           (tensor_cores == 3 || (tensor_cores == 0 && d->N == 4 && d->d == 4)) &&
           ammmse::tc2::shape_ok(d->M, d->K * d->N, ncol)) {
-        const int st = e->tc2_stages(d->M, d->K, c, (size_t)lim - 256);  // static shared: ctl, mbarriers
+        const int st = e->tc2_stages(d->M, d->K, c, (size_t)lim - 2048);  // static shared: ctl, barriers, exchange copy
         if (st >= 2) {
           p->cluster = c;
           p->hres = 0;
